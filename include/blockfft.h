@@ -1,0 +1,220 @@
+/*
+ * blockfft.h — C ABI of the B200-native per-record FFT (arXiv 1407.6915).
+ *
+ * The method (§III): a very large signal file is split into
+ * fixed-length records ("FFT segments"), each record is
+ * transformed independently by a Cooley–Tukey FFT (§I), the
+ * transform is run as one batched plan over many records at once
+ * ("partitioning of FFT segments can be done inside memory using CUFFT's
+ * batched FFT plan"), and the outputs are written back in file
+ * order ("named by their position in the original file").
+ *
+ * Conventions:
+ *   - A record is N complex64 samples: interleaved little-endian float32
+ *     (re, im), record-major, 8*N bytes (reading c1).
+ *   - N is a power of two, 2 <= N <= 2^22 (reading c7).
+ *   - FFT_FORWARD: X[k] = sum_j x[j] exp(-2 pi i jk/N), unnormalised.
+ *     FFT_INVERSE: x[j] = (1/N) sum_k X[k] exp(+2 pi i jk/N)
+ *     (readings c2/c3).
+ *   - Bin k of a record's transform is at index k (natural order, c4).
+ *
+ * Every entry point is thread-safe.  Errors: functions returning int return
+ * FFT_OK (0) or one of the FFT_E_* codes; functions returning a pointer
+ * return NULL.  In both cases fft_last_error() returns a thread-local message
+ * naming the offending value ("unsupported transform size" naming
+ * the value; "expected vs actual").
+ *
+ * Nothing in this header depends on PyTorch; device pointers are plain CUDA
+ * device pointers and streams are cudaStream_t passed as void*.
+ */
+#ifndef BLOCKFFT_H
+#define BLOCKFFT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BLOCKFFT_VERSION 1
+
+#define FFT_FORWARD (-1) /* exp(-2 pi i jk/N), unnormalised  */
+#define FFT_INVERSE (+1) /* exp(+2 pi i jk/N), scaled by 1/N     */
+
+enum fft_status {
+    FFT_OK = 0,
+    FFT_E_SIZE = 1,   /* N not a power of two in [2, 2^22]                     */
+    FFT_E_BATCH = 2,  /* batch < 1                                            */
+    FFT_E_DIR = 3,    /* direction not -1 / +1                                */
+    FFT_E_ARG = 4,    /* NULL / misaligned / partially overlapping pointers   */
+    FFT_E_DEVICE = 5, /* no such device, or plan used on another device       */
+    FFT_E_CUDA = 6,   /* a CUDA runtime call failed (message has its text)    */
+    FFT_E_NOMEM = 7,  /* device or pinned host allocation failed              */
+    FFT_E_IO = 8,     /* open/read/write/rename failed, or short read         */
+    FFT_E_EMPTY = 9   /* empty input file                       */
+};
+
+/* Kernel variant of a plan.                           */
+enum fft_variant {
+    FFT_VARIANT_AUTO = 0,     /* choose by N (the default)                    */
+    FFT_VARIANT_SINGLE = 1,   /* one kernel, record in one CTA, N <= 2^14      */
+    FFT_VARIANT_CLUSTER = 2,  /* one kernel, record across a CTA cluster
+                                 exchanging through DSMEM, 2^10 <= N <= 2^17   */
+    FFT_VARIANT_FOURSTEP = 3, /* two kernels (column FFT + twiddle, row FFT +
+                                 transposed store) through HBM scratch, N >= 4 */
+    FFT_VARIANT_IDENTITY = 4  /* copy kernel: out = in bit-exactly (pipeline
+                                 test mode)                      */
+};
+
+typedef struct fft_plan fft_plan; /* opaque */
+
+/*
+ * fft_plan_create — the batched plan ("CUFFT's batched FFT plan";
+ * SURVEY.md §8(a) row a1; SPEC.md:42-50 plan_create).
+ *   n     transform length N (power of two, 2..2^22), else FFT_E_SIZE
+ *         ("unsupported transform size: <n>").
+ *   batch number of records per fft_exec call (>= 1), else FFT_E_BATCH.
+ *   dir   FFT_FORWARD or FFT_INVERSE, else FFT_E_DIR.
+ * The plan is bound to the CUDA device current at creation.  It owns its
+ * device twiddle tables (computed in fp64 on the host, rounded once to fp32)
+ * and, for the four-step variant, an HBM scratch buffer of batch*8*N bytes
+ * (or of one wave, see fft_plan_info).  Synchronous; allocates.
+ * Returns NULL on error (see fft_last_error()).
+ */
+fft_plan *fft_plan_create(int64_t n, int64_t batch, int dir);
+
+/* As fft_plan_create with an explicit kernel variant (enum fft_variant).
+ * A variant that cannot handle n fails with FFT_E_SIZE.                     */
+fft_plan *fft_plan_create_ex(int64_t n, int64_t batch, int dir, int variant);
+
+/*
+ * fft_exec — transform `batch` records.
+ *   in, out  device pointers to batch*N complex64 values, 16-byte aligned,
+ *            caller-owned.  in == out (in place) is allowed; partial overlap
+ *            is FFT_E_ARG.
+ *   stream   cudaStream_t (as void*; NULL = legacy default stream).
+ * Enqueues the plan's kernels on `stream` and returns: no allocation, no host
+ * synchronisation, no host<->device copy — graph-capturable.  Argument errors
+ * are returned synchronously; launch errors as FFT_E_CUDA; device faults
+ * surface at the caller's next synchronisation.  Single-kernel plans may run
+ * concurrently on several streams; a four-step plan owns scratch and must not
+ * run concurrently with itself (create one plan per stream).
+ */
+int fft_exec(const fft_plan *plan, const void *in, void *out, void *stream);
+
+/* Like fft_exec on the first `count` records at in/out (1 <= count <= batch);
+ * the caller offsets the pointers.  Used by the streamer for partial chunks. */
+int fft_exec_range(const fft_plan *plan, const void *in, void *out, int64_t count, void *stream);
+
+/* Release a plan (NULL-safe).  The caller must have synchronised every stream
+ * the plan was executed on.                                                  */
+void fft_plan_destroy(fft_plan *plan);
+
+typedef struct fft_plan_info {
+    int64_t n, batch;
+    int dir;
+    int variant;          /* enum fft_variant actually used                    */
+    int kernels_per_exec; /* kernel launches one fft_exec enqueues            */
+    int device;
+    int64_t n1, n2;       /* four-step / cluster split N = n1*n2 (else n, 1)   */
+    int cluster;          /* CTAs per cluster (cluster variant), else 1        */
+    int64_t scratch_bytes;/* HBM scratch owned by the plan                     */
+    int64_t table_bytes;  /* device twiddle tables owned by the plan           */
+} fft_plan_info;
+
+/* Fill *info for a plan.  Returns FFT_OK or FFT_E_ARG.                       */
+int fft_plan_get_info(const fft_plan *plan, fft_plan_info *info);
+
+/*
+ * Partitioner (SURVEY.md §8(a) row a7; PAPER.md:49 "offset", :53 one block
+ * per map task, :63 outputs named by position; SPEC.md:141-149 split_plan).
+ * fft_file_records: R = ceil(file_bytes / (8*record_len)) records (the final
+ *   record zero-padded).  Returns R, or -FFT_E_* (< 0).
+ * fft_partition: contiguous range of part `part` of `nparts`:
+ *   first = floor(part*R/nparts), count = floor((part+1)*R/nparts) - first.
+ *   All arithmetic is int64 (2^40-byte files overflow 32 bits).
+ *   Returns FFT_OK or FFT_E_ARG.
+ */
+int64_t fft_file_records(int64_t file_bytes, int64_t record_len);
+int fft_partition(int64_t total_records, int nparts, int part, int64_t *first, int64_t *count);
+
+typedef struct fft_stream_opts {
+    int64_t chunk_bytes;  /* bytes per pipeline chunk (the paper's block,
+                             PAPER.md:55-61 dfs.block.size); 0 = default 256 MiB,
+                             or env BLOCKFFT_CHUNK_BYTES                         */
+    int depth;            /* pipeline buffers per stage (>= 2); 0 = default 3  */
+    int variant;          /* enum fft_variant for the per-chunk plan (0=auto)  */
+    int io_threads;       /* host I/O threads per GPU for file pread/pwrite; 0 = 4 */
+} fft_stream_opts;
+
+typedef struct fft_stream_stats {
+    int64_t records;      /* records transformed (all GPUs)                     */
+    int64_t chunks;       /* chunks processed (all GPUs)                        */
+    int64_t bytes_in;     /* input bytes moved host->device                     */
+    int64_t bytes_out;    /* output bytes moved device->host                    */
+    double wall_s;        /* first read to last write                           */
+    double read_s;        /* summed per-chunk host read time (file source)      */
+    double h2d_s;         /* summed per-chunk H2D copy time (CUDA events)       */
+    double fft_s;         /* summed per-chunk kernel time (CUDA events)         */
+    double d2h_s;         /* summed per-chunk D2H copy time (CUDA events)       */
+    double write_s;       /* summed per-chunk host write time (file sink)       */
+    int ngpu;
+} fft_stream_stats;
+
+/*
+ * fft_file — the whole method on a file (north_star; §III).
+ *   in_path      headerless complex64 little-endian file; size must be a
+ *                multiple of 8 bytes (else FFT_E_ARG); empty -> FFT_E_EMPTY.
+ *   out_path     written as out_path + ".tmp" then renamed; its
+ *                size is R*8*record_len with the final record zero-padded
+ *                (SPEC.md:188).  On failure the .tmp is removed and out_path
+ *                is untouched.
+ *   record_len   N, validated as in fft_plan_create.
+ *   ngpu         devices 0..ngpu-1 (1 <= ngpu <= device count, else
+ *                FFT_E_DEVICE).  GPU g transforms the contiguous record range
+ *                fft_partition(R, ngpu, g) and writes it at byte offset
+ *                first*8*N of the output — no merge step, no collective
+ *                (PAPER.md:63 zero reducers; reading c5).
+ * Forward direction.  Per GPU: pread -> pinned buffer -> H2D (copy stream) ->
+ * fft_exec (compute stream) -> D2H (second copy stream) -> pwrite, `depth`
+ * chunks in flight so copies overlap compute in both directions
+ * (SURVEY.md §8(a) row a8).
+ */
+int fft_file(const char *in_path, const char *out_path, int64_t record_len, int ngpu);
+
+/* fft_file with direction, options (may be NULL) and stats (may be NULL).
+ * dir may also be 0 for the identity kernel (bit-exact copy).  */
+int fft_file_ex(const char *in_path, const char *out_path, int64_t record_len, int ngpu,
+                int dir, const fft_stream_opts *opts, fft_stream_stats *stats);
+
+/*
+ * fft_exec_host — transform `batch` records held in HOST memory on one GPU
+ * through the same chunked, overlapped streamer as fft_file (memory source
+ * and sink instead of a file).
+ *   host_in, host_out  host pointers, batch*8*n bytes each; may be equal.
+ *                      Pinned (cudaHostAlloc / registered) buffers are copied
+ *                      directly; pageable ones are staged through the
+ *                      streamer's pinned ring.
+ *   device             CUDA device index.
+ *   dir                FFT_FORWARD, FFT_INVERSE, or 0 (identity).
+ * Synchronous: returns when host_out holds the result.
+ */
+int fft_exec_host(int64_t n, int64_t batch, int dir, const void *host_in, void *host_out,
+                  int device, const fft_stream_opts *opts, fft_stream_stats *stats);
+
+/* Thread-local message describing the last error on this thread ("" if none). */
+const char *fft_last_error(void);
+
+/* Thread-local FFT_* status of the last failed call on this thread (FFT_OK if
+ * the last call succeeded); lets callers of the pointer-returning
+ * fft_plan_create recover the code.                                          */
+int fft_last_status(void);
+
+/* BLOCKFFT_VERSION of the loaded library. */
+int fft_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BLOCKFFT_H */

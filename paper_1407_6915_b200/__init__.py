@@ -1,0 +1,198 @@
+"""paper_1407_6915_b200 — B200-native per-record FFT over very large signal files
+(arXiv 1407.6915, "Accelerating Fast Fourier Transforms Using Hadoop and CUDA").
+
+Thin Python layer over the C ABI in ``include/blockfft.h`` (``libblockfft.so``):
+argument marshalling only; every step of the transform runs in the library's
+sm_100a kernels.  PyTorch is used for device memory and streams.
+
+    import paper_1407_6915_b200 as bf
+    plan = bf.Plan(n=65536, batch=8192)          # fft_plan_create
+    plan.exec(x, y)                              # fft_exec on the current stream
+    bf.fft_file("in.c64", "out.c64", 1024, ngpu=2)   # the whole method on a file
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import _abi
+from ._abi import (FFT_FORWARD, FFT_IDENTITY, FFT_INVERSE, VARIANT_AUTO, VARIANT_CLUSTER,  # noqa: F401
+                   VARIANT_FOURSTEP, VARIANT_IDENTITY, VARIANT_NAMES, VARIANT_SINGLE)
+
+_lib = _abi.lib
+
+
+class FFTError(RuntimeError):
+    """A libblockfft call failed; ``code`` is the FFT_E_* status."""
+
+    def __init__(self, code: int, msg: str):
+        self.code = code
+        name = _abi.STATUS_NAMES[code] if 0 <= code < len(_abi.STATUS_NAMES) else str(code)
+        super().__init__(f"{name}: {msg}")
+
+
+def last_error() -> str:
+    return (_lib.fft_last_error() or b"").decode()
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise FFTError(rc, last_error())
+
+
+def version() -> int:
+    return int(_lib.fft_version())
+
+
+class Plan:
+    """Batched plan: ``batch`` records of ``n`` complex64 points (fft_plan_create).
+
+    Bound to the CUDA device current at construction.  ``exec`` enqueues on the
+    current torch stream (or ``stream``) and returns immediately.
+    """
+
+    def __init__(self, n: int, batch: int, direction: int = FFT_FORWARD,
+                 variant: int = VARIANT_AUTO, device=None):
+        import torch
+        self.n, self.batch, self.direction = int(n), int(batch), int(direction)
+        if device is not None:
+            torch.cuda.set_device(device)
+        self.device = torch.cuda.current_device() if torch.cuda.is_available() else None
+        h = _lib.fft_plan_create_ex(self.n, self.batch, self.direction, int(variant))
+        if not h:
+            raise FFTError(int(_lib.fft_last_status()), last_error())
+        self._h = ctypes.c_void_p(h)
+
+    def info(self) -> dict:
+        inf = _abi.PlanInfo()
+        _check(_lib.fft_plan_get_info(self._h, ctypes.byref(inf)))
+        d = {name: getattr(inf, name) for name, _ in inf._fields_}
+        d["variant_name"] = VARIANT_NAMES.get(d["variant"], "?")
+        return d
+
+    def _validate(self, t, name, count):
+        import torch
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{name} must be a torch.Tensor")
+        if t.dtype != torch.complex64:
+            raise ValueError(f"{name}: expected dtype complex64, got {t.dtype}")
+        if not t.is_cuda:
+            raise ValueError(f"{name}: expected a CUDA tensor")
+        if not t.is_contiguous():
+            raise ValueError(f"{name}: expected a contiguous tensor")
+        if t.numel() != count * self.n or (t.dim() == 2 and tuple(t.shape) != (count, self.n)):
+            raise ValueError(f"{name}: expected (B,N)=({count},{self.n}) got {tuple(t.shape)}")
+
+    def exec(self, x, out=None, stream=None, count: int | None = None):
+        """Transform ``count`` (default: batch) records of x into out (default:
+        in place).  Returns out."""
+        import torch
+        count = self.batch if count is None else int(count)
+        if out is None:
+            out = x
+        self._validate(x, "input", count)
+        self._validate(out, "output", count)
+        s = stream if stream is not None else torch.cuda.current_stream()
+        rc = _lib.fft_exec_range(self._h, ctypes.c_void_p(x.data_ptr()),
+                                 ctypes.c_void_p(out.data_ptr()), count,
+                                 ctypes.c_void_p(s.cuda_stream))
+        _check(rc)
+        return out
+
+    __call__ = exec
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.fft_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def fft(x, direction: int = FFT_FORWARD, variant: int = VARIANT_AUTO, out=None):
+    """One-shot batched FFT of a (B, N) complex64 CUDA tensor (plan per call)."""
+    b, n = x.shape
+    with Plan(n, b, direction, variant) as p:
+        if out is None:
+            import torch
+            out = torch.empty_like(x)
+        p.exec(x, out)
+        import torch
+        torch.cuda.current_stream().synchronize()
+    return out
+
+
+def _opts(chunk_bytes=0, depth=0, variant=VARIANT_AUTO, io_threads=0):
+    return _abi.StreamOpts(int(chunk_bytes), int(depth), int(variant), int(io_threads))
+
+
+def fft_file(in_path: str, out_path: str, record_len: int, ngpu: int = 1,
+             direction: int = FFT_FORWARD, chunk_bytes: int = 0, depth: int = 0,
+             variant: int = VARIANT_AUTO) -> dict:
+    """The whole method on a file (fft_file_ex).  Returns the stream stats."""
+    st = _abi.StreamStats()
+    o = _opts(chunk_bytes, depth, variant)
+    rc = _lib.fft_file_ex(os.fsencode(in_path), os.fsencode(out_path), int(record_len), int(ngpu),
+                          int(direction), ctypes.byref(o), ctypes.byref(st))
+    _check(rc)
+    return st.as_dict()
+
+
+def exec_host(x_host, n: int, direction: int = FFT_FORWARD, device: int = 0, out=None,
+              chunk_bytes: int = 0, depth: int = 0, variant: int = VARIANT_AUTO) -> dict:
+    """Transform records held in host memory (torch CPU tensor, pinned or not,
+    or numpy array) through the streamer (fft_exec_host).  In place unless
+    ``out`` is given.  Returns the stream stats."""
+    if out is None:
+        out = x_host
+    ptr_in, nbytes = _host_ptr(x_host)
+    ptr_out, nbytes_o = _host_ptr(out)
+    if nbytes != nbytes_o or nbytes % (8 * n):
+        raise ValueError(f"expected equal host buffers of a multiple of {8 * n} bytes, got {nbytes} / {nbytes_o}")
+    st = _abi.StreamStats()
+    o = _opts(chunk_bytes, depth, variant)
+    rc = _lib.fft_exec_host(int(n), nbytes // (8 * n), int(direction), ctypes.c_void_p(ptr_in),
+                            ctypes.c_void_p(ptr_out), int(device), ctypes.byref(o), ctypes.byref(st))
+    _check(rc)
+    return st.as_dict()
+
+
+def _host_ptr(a):
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            if a.is_cuda or not a.is_contiguous():
+                raise ValueError("expected a contiguous CPU tensor")
+            return a.data_ptr(), a.numel() * a.element_size()
+    except ImportError:
+        pass
+    import numpy as np
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("expected a C-contiguous array")
+        return a.ctypes.data, a.nbytes
+    raise TypeError("expected a torch CPU tensor or numpy array")
+
+
+def file_records(file_bytes: int, record_len: int) -> int:
+    r = int(_lib.fft_file_records(int(file_bytes), int(record_len)))
+    if r < 0:
+        raise FFTError(-r, last_error())
+    return r
+
+
+def partition(total_records: int, nparts: int, part: int) -> tuple[int, int]:
+    """(first, count) of part `part` of `nparts` contiguous record ranges."""
+    f, c = ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib.fft_partition(int(total_records), int(nparts), int(part), ctypes.byref(f), ctypes.byref(c)))
+    return f.value, c.value

@@ -1,0 +1,72 @@
+"""Build the in-tree native libraries (no JIT cache; the .so files travel to
+the GPU box with the repo snapshot).
+
+  paper_1407_6915_b200/libblockfft.so  — the C-ABI product library
+      csrc/plan.cu (plan layer + kernels), csrc/stream.cpp (streamer)
+  synth/libsynth.so                    — seeded CUDA fill kernel (inputs only)
+
+All CUDA code is compiled for sm_100a only:
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo (no fast-math).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INC = os.path.join(ROOT, "include")
+BUILD = os.path.join(ROOT, "build")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+LIB = os.path.join(PKG, "libblockfft.so")
+SYNTH_LIB = os.path.join(ROOT, "synth", "libsynth.so")
+
+
+def _newer(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd):
+    print("+", " ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd)
+
+
+def build(force: bool = False, verbose_ptxas: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    headers.append(os.path.join(INC, "blockfft.h"))
+    objs = []
+    for src, kind in (("plan.cu", "cu"), ("stream.cpp", "cpp")):
+        s = os.path.join(CSRC, src)
+        o = os.path.join(BUILD, src + ".o")
+        objs.append(o)
+        if force or _newer(o, [s] + headers):
+            if kind == "cu":
+                cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                       "-I", INC, "-c", s, "-o", o]
+                if verbose_ptxas:
+                    cmd[1:1] = ["-Xptxas", "-v"]
+            else:
+                cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-I", INC,
+                       "-I", os.path.join(CUDA, "include"), "-c", s, "-o", o]
+            _run(cmd)
+    if force or _newer(LIB, objs):
+        _run([NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lcudart", "-lpthread"])
+        os.replace(LIB + ".tmp", LIB)
+    ssrc = os.path.join(ROOT, "synth", "csrc", "synth_fill.cu")
+    if force or _newer(SYNTH_LIB, [ssrc]):
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", ssrc,
+              "-o", SYNTH_LIB + ".tmp", "-lcudart"])
+        os.replace(SYNTH_LIB + ".tmp", SYNTH_LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv)

@@ -1,0 +1,350 @@
+// fft_kernels.cuh — the sm_100a kernels of the per-record FFT.
+//
+//   k_rows      engine E1: single-pass Stockham, B whole records per CTA
+//               (SURVEY.md §8(a) rows a2, a3, a5, a6).
+//   k_fs_cols   four-step pass A: length-N1 FFTs down the columns of the
+//               record viewed as [N1][N2], times W_N^{n2 k1} (row a4).
+//   k_fs_rows   four-step pass B: length-N2 FFTs along the rows, stored
+//               transposed to X[k1 + N1 k2] (row a4).
+//   k_cluster   cluster variant: the four-step of row a4 inside one thread
+//               block cluster, the transpose an all-to-all through DSMEM
+//               (row a3'), so a record is read and written once.
+//   k_copy      identity kernel (SPEC.md:275 test mode).
+//
+// The four-step split (north_star): with
+//   n = N2*n1 + n2 and k = k1 + N1*k2,
+//   X[k1 + N1 k2] = sum_n2 W_N2^{n2 k2} [ W_N^{n2 k1} sum_n1 x[N2 n1 + n2] W_N1^{n1 k1} ].
+#pragma once
+
+#include <type_traits>
+
+#include "fft_device.cuh"
+
+namespace bfft {
+
+// ------------------------------------------------------------ small helpers
+template <int I, int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+    if constexpr (I < N) {
+        f(std::integral_constant<int, I>{});
+        static_for<I + 1, N>(f);
+    }
+}
+
+__device__ __forceinline__ float2 ld_stream(const float2* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(float2* p, float2 v) { __stcs(p, v); }
+
+// W_N^m = exp(-2 pi i m / N) from fp64 sincospi, rounded once to fp32.
+__device__ __forceinline__ float2 twiddle_exact(uint32_t m, uint32_t n) {
+    double s, c;
+    sincospi(-2.0 * (double)m / (double)n, &s, &c);
+    return make_float2((float)c, (float)s);
+}
+
+// Per-pass Stockham twiddle fetch: table layout [q-1][j mod Ns] per pass.
+template <int L>
+struct TableTw {
+    const float2* __restrict__ base;  // this length's table
+    template <int PASS>
+    __device__ __forceinline__ float2 get(int q, int jj) const {
+        return __ldg(base + Sched<L>::tw_off(PASS) + (q - 1) * Sched<L>::ns(PASS) + jj);
+    }
+};
+
+// Run every pass of a length-L transform on v (v[s] = x[t + s*T] on entry,
+// v[q] = X[t + q*T] on exit).  Intermediate passes exchange through `sm`
+// addressed by addr(e) (the caller's layout).  Begins each exchange with a
+// CTA barrier, so the buffer may still be read by other threads on entry.
+template <int L, class Addr>
+__device__ __forceinline__ void fft_engine(float2 (&v)[Sched<L>::P], int t, float2* sm,
+                                           Addr&& addr, const TableTw<L>& tw) {
+    using S = Sched<L>;
+    constexpr int P = S::P, T = S::T;
+    static_for<0, S::NPASS>([&](auto pc) {
+        constexpr int PASS = decltype(pc)::value;
+        auto twf = [&](int q, int jj) { return tw.template get<PASS>(q, jj); };
+        if constexpr (PASS == S::NPASS - 1) {
+            float2 o[P];
+            stockham_pass<L, PASS>(v, t, [&](int, int q, int, float2 val) { o[q] = val; }, twf);
+#pragma unroll
+            for (int q = 0; q < P; ++q) v[q] = o[q];
+        } else {
+            __syncthreads();
+            stockham_pass<L, PASS>(v, t, [&](int idx, int, int, float2 val) { sm[addr(idx)] = val; }, twf);
+            __syncthreads();
+#pragma unroll
+            for (int s = 0; s < P; ++s) v[s] = sm[addr(t + s * T)];
+        }
+    });
+}
+
+// w[q] = W_N^{m0 + q*dm} for q = 0..15 (mod N), as b * s1^a * s2^b * s4^c * s8^d
+// with every factor from fp64 sincospi: at most four fp32 products per value.
+__device__ __forceinline__ void twiddle_row16(uint32_t m0, uint32_t dm, uint32_t nmask, uint32_t n,
+                                              float2 (&w)[16]) {
+    const float2 b = twiddle_exact(m0 & nmask, n);
+    const float2 s1 = twiddle_exact(dm & nmask, n);
+    const float2 s2 = twiddle_exact((2u * dm) & nmask, n);
+    const float2 s4 = twiddle_exact((4u * dm) & nmask, n);
+    const float2 s8 = twiddle_exact((8u * dm) & nmask, n);
+    w[0] = b;
+    w[1] = cmul(b, s1);
+    w[2] = cmul(b, s2);
+    w[3] = cmul(w[1], s2);
+#pragma unroll
+    for (int q = 4; q < 8; ++q) w[q] = cmul(w[q - 4], s4);
+#pragma unroll
+    for (int q = 8; q < 16; ++q) w[q] = cmul(w[q - 8], s8);
+}
+
+// ======================================================================
+// E1: single-pass, B records per CTA, one record = T threads x P points.
+// ======================================================================
+template <int L, int B, bool INV>
+__global__ void __launch_bounds__(B * Sched<L>::T)
+k_rows(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
+       const float2* __restrict__ tw, float scale) {
+    using S = Sched<L>;
+    constexpr int P = S::P, T = S::T;
+    extern __shared__ float2 sm[];
+    const int tid = threadIdx.x;
+    const int b = tid / T, t = tid - (tid / T) * T;
+    const TableTw<L> tab{tw};
+    auto addr = [&](int e) { return RowLayout::at(b * L + e); };
+    for (int64_t g = blockIdx.x; g * B < nrec; g += gridDim.x) {
+        const int64_t r = g * B + b;
+        const bool ok = r < nrec;
+        const float2* src = in + r * (int64_t)L + t;
+        float2 v[P];
+#pragma unroll
+        for (int s = 0; s < P; ++s) {
+            float2 x = ok ? ld_stream(src + s * T) : make_float2(0.f, 0.f);
+            v[s] = INV ? conjf2(x) : x;
+        }
+        fft_engine<L>(v, t, sm, addr, tab);
+        if (ok) {
+            float2* dst = out + r * (int64_t)L + t;
+#pragma unroll
+            for (int q = 0; q < P; ++q) st_stream(dst + q * T, INV ? scale_conj(v[q], scale) : v[q]);
+        }
+    }
+}
+
+// ======================================================================
+// Four-step pass A: for a tile of COLS adjacent columns n2 of record r,
+// Y[k1][n2] = W_N^{n2 k1} * FFT_N1 over n1 of x[N2 n1 + n2].
+// ======================================================================
+template <int N1, int COLS, bool INV>
+__global__ void __launch_bounds__(COLS * Sched<N1>::T)
+k_fs_cols(const float2* __restrict__ in, float2* __restrict__ y, int64_t nrec, int log2n2,
+          const float2* __restrict__ tw) {
+    using S = Sched<N1>;
+    constexpr int P = S::P, T = S::T;
+    extern __shared__ float2 sm[];
+    const int tid = threadIdx.x;
+    const int col = tid % COLS, t = tid / COLS;
+    const int n2 = 1 << log2n2;
+    const int tiles = n2 / COLS;
+    const uint32_t n = (uint32_t)N1 << log2n2, nmask = n - 1;
+    const TableTw<N1> tab{tw};
+    auto addr = [&](int e) { return ColLayout<COLS>::at(e, col); };
+    for (int64_t g = blockIdx.x; g < nrec * tiles; g += gridDim.x) {
+        const int64_t r = g / tiles;
+        const int c = (int)(g - r * tiles) * COLS + col;     // this thread's n2
+        const float2* src = in + r * (int64_t)n + c + (int64_t)t * n2;
+        float2 v[P];
+#pragma unroll
+        for (int s = 0; s < P; ++s) {
+            float2 x = ld_stream(src + (int64_t)s * T * n2);
+            v[s] = INV ? conjf2(x) : x;
+        }
+        fft_engine<N1>(v, t, sm, addr, tab);
+        float2 w[16];
+        // k1 = t + q*T  ->  W_N^{n2 (t + q T)}
+        twiddle_row16((uint32_t)c * (uint32_t)t, (uint32_t)c * (uint32_t)T, nmask, n, w);
+        float2* dst = y + r * (int64_t)n + c + (int64_t)t * n2;
+#pragma unroll
+        for (int q = 0; q < P; ++q) dst[(int64_t)q * T * n2] = cmul(v[q], w[q]);
+    }
+}
+
+// ======================================================================
+// Four-step pass B: for ROWS adjacent rows k1 of Y (record r), FFT_N2 along
+// n2 and store X[k1 + N1 k2].  The tile is loaded coalesced along n2 and
+// transposed into the column layout through shared memory.
+// ======================================================================
+template <int N2, int ROWS, bool INV>
+__global__ void __launch_bounds__(ROWS * Sched<N2>::T)
+k_fs_rows(const float2* __restrict__ y, float2* __restrict__ out, int64_t nrec, int log2n1,
+          const float2* __restrict__ tw, float scale) {
+    using S = Sched<N2>;
+    constexpr int P = S::P, T = S::T;
+    constexpr int NT = ROWS * T;
+    extern __shared__ float2 sm[];
+    const int tid = threadIdx.x;
+    const int col = tid % ROWS, t = tid / ROWS;
+    const int n1 = 1 << log2n1;
+    const int tiles = n1 / ROWS;
+    const int64_t n = (int64_t)n1 * N2;
+    const TableTw<N2> tab{tw};
+    auto addr = [&](int e) { return ColLayout<ROWS>::at(e, col); };
+    for (int64_t g = blockIdx.x; g < nrec * tiles; g += gridDim.x) {
+        const int64_t r = g / tiles;
+        const int k0 = (int)(g - r * tiles) * ROWS;
+        const float2* src = y + r * n + (int64_t)k0 * N2;
+        __syncthreads();  // previous tile fully consumed
+#pragma unroll
+        for (int u = 0; u < P; ++u) {
+            const int i = tid + u * NT;          // linear index in the ROWS x N2 tile
+            const int row = i / N2, e = i - (i / N2) * N2;
+            sm[ColLayout<ROWS>::at(e, row)] = ld_stream(src + i);
+        }
+        __syncthreads();
+        float2 v[P];
+#pragma unroll
+        for (int s = 0; s < P; ++s) v[s] = sm[addr(t + s * T)];
+        fft_engine<N2>(v, t, sm, addr, tab);
+        float2* dst = out + r * n + k0 + col + (int64_t)t * n1;
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+            st_stream(dst + (int64_t)q * T * n1, INV ? scale_conj(v[q], scale) : v[q]);
+    }
+}
+
+// ======================================================================
+// Cluster variant.  A cluster of C CTAs owns one record at a time
+// (persistent over records).  CTA `rank` computes phase A for columns
+// n2 in [rank*CA, (rank+1)*CA) (CA = N2/C) and pushes Y[k1][n2] straight
+// into the shared memory of CTA k1 / CB (CB = N1/C), which then computes
+// phase B for rows k1 in its range and stores X[k1 + N1 k2].
+// ======================================================================
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t map_rank(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster(uint32_t addr, float2 v) {
+    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t ncluster_x() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+    return r;
+}
+
+template <int N1, int N2, int C>
+struct ClusterCfg {
+    static constexpr int N = N1 * N2;
+    static constexpr int CA = N2 / C;   // phase-A columns per CTA
+    static constexpr int CB = N1 / C;   // phase-B columns (rows k1) per CTA
+    static constexpr int NT = N / (16 * C);
+    static constexpr int TA = Sched<N1>::T, TB = Sched<N2>::T;
+    static_assert(Sched<N1>::P == 16 && Sched<N2>::P == 16, "cluster variant needs N1, N2 >= 16");
+    static_assert(CA * TA == NT && CB * TB == NT, "thread mapping");
+    static_assert(CA >= 16 && CB >= 16, "column tiles of >= 16 keep shared accesses conflict-free");
+    static constexpr size_t SMEM = 2 * sizeof(float2) * (N / C);  // work + recv
+};
+
+template <int N1, int N2, int C, bool INV>
+__global__ void __launch_bounds__(ClusterCfg<N1, N2, C>::NT)
+k_cluster(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
+          const float2* __restrict__ tw1, const float2* __restrict__ tw2, float scale) {
+    using CF = ClusterCfg<N1, N2, C>;
+    constexpr int N = CF::N, CA = CF::CA, CB = CF::CB, TA = CF::TA, TB = CF::TB;
+    extern __shared__ float2 sm[];
+    float2* work = sm;             // phase-A exchange buffer, N/C entries
+    float2* recv = sm + N / C;     // phase-B input (written by all ranks) and exchange
+    const int tid = threadIdx.x;
+    const uint32_t rank = cluster_rank();
+    const int64_t cid = cluster_id_x(), ncl = ncluster_x();
+
+    // phase-A mapping: column n2, butterfly row tA
+    const int colA = tid % CA, tA = tid / CA;
+    const int n2 = (int)rank * CA + colA;
+    // phase-B mapping: column k1 (local kb), butterfly row tB
+    const int colB = tid % CB, tB = tid / CB;
+    const int k1b = (int)rank * CB + colB;
+
+    // W_N^{n2 k1} for this thread's k1 = tA + q*TA: fixed for the whole kernel.
+    float2 w4[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+        w4[q] = twiddle_exact(((uint32_t)n2 * (uint32_t)(tA + q * TA)) & (N - 1), N);
+
+    // Remote base of every destination's recv buffer, and this thread's
+    // destination offsets: Y[k1][n2] -> rank k1/CB, recv[ColLayout<CB>(n2, k1 % CB)].
+    const uint32_t recv_local = smem_addr(recv);
+    uint32_t dst_addr[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const int k1 = tA + q * TA;
+        const uint32_t dst_rank = (uint32_t)(k1 / CB);
+        dst_addr[q] = map_rank(recv_local, dst_rank) +
+                      (uint32_t)(ColLayout<CB>::at(n2, k1 % CB) * sizeof(float2));
+    }
+    const TableTw<N1> tabA{tw1};
+    const TableTw<N2> tabB{tw2};
+    auto addrA = [&](int e) { return ColLayout<CA>::at(e, colA); };
+    auto addrB = [&](int e) { return ColLayout<CB>::at(e, colB); };
+
+    cluster_arrive();  // "recv is free" for the first record
+    for (int64_t r = cid; r < nrec; r += ncl) {
+        // ---- phase A: column FFTs of length N1 over n1, times W_N^{n2 k1}
+        const float2* src = in + r * N + n2 + (int64_t)tA * N2;
+        float2 v[16];
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            float2 x = ld_stream(src + s * TA * N2);
+            v[s] = INV ? conjf2(x) : x;
+        }
+        fft_engine<N1>(v, tA, work, addrA, tabA);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = cmul(v[q], w4[q]);
+        // ---- exchange: all-to-all through distributed shared memory
+        cluster_wait();    // every rank finished reading its recv for record r - ncl
+#pragma unroll
+        for (int q = 0; q < 16; ++q) st_cluster(dst_addr[q], v[q]);
+        cluster_arrive();
+        cluster_wait();    // all pushes for record r have landed
+        // ---- phase B: row FFTs of length N2 over n2, stored to X[k1 + N1 k2]
+#pragma unroll
+        for (int s = 0; s < 16; ++s) v[s] = recv[addrB(tB + s * TB)];
+        fft_engine<N2>(v, tB, recv, addrB, tabB);
+        cluster_arrive();  // this thread is done with recv
+        float2* dst = out + r * N + k1b + (int64_t)tB * N1;
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+            st_stream(dst + (int64_t)q * TB * N1, INV ? scale_conj(v[q], scale) : v[q]);
+    }
+    cluster_wait();
+}
+
+// ======================================================================
+// Identity kernel: out = in, bit-exact, 16-byte vectors.
+// ======================================================================
+__global__ void k_copy(const float4* __restrict__ in, float4* __restrict__ out, int64_t n16) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16;
+         i += (int64_t)gridDim.x * blockDim.x)
+        __stcs(out + i, __ldcs(in + i));
+}
+
+}  // namespace bfft

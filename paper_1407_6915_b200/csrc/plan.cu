@@ -1,0 +1,507 @@
+// plan.cu — the C ABI's plan layer: fft_plan_create / fft_exec / fft_plan_destroy
+// (include/blockfft.h).
+//
+// PAPER.md:53 §III moves each block to the GPU and runs "CUFFT's batched FFT
+// plan" over it; here the batched plan is our own: validation, variant choice
+// by N, fp64-computed twiddle tables rounded once to fp32 and uploaded, launch
+// geometry, and (four-step) an HBM scratch wave.  fft_exec only enqueues.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/blockfft.h"
+#include "common.h"
+#include "fft_kernels.cuh"
+
+using namespace bfft;
+
+// ------------------------------------------------------------ error state
+static thread_local std::string g_err;
+static thread_local int g_code = 0;
+
+int bfft_set_error(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    g_code = code;
+    return code;
+}
+void bfft_clear_error() {
+    g_err.clear();
+    g_code = 0;
+}
+int bfft_last_code() { return g_code ? g_code : FFT_E_CUDA; }
+
+extern "C" const char* fft_last_error(void) { return g_err.c_str(); }
+extern "C" int fft_last_status(void) { return g_code; }
+extern "C" int fft_version(void) { return BLOCKFFT_VERSION; }
+
+#define CUDA_TRY(call)                                                                          \
+    do {                                                                                        \
+        cudaError_t e_ = (call);                                                                \
+        if (e_ != cudaSuccess)                                                                  \
+            return bfft_set_error(FFT_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+// ------------------------------------------------------------ kernel tables
+using RowFn = void (*)(const float2*, float2*, int64_t, const float2*, float);
+using ColFn = void (*)(const float2*, float2*, int64_t, int, const float2*);
+using RowTFn = void (*)(const float2*, float2*, int64_t, int, const float2*, float);
+using ClusterFn = void (*)(const float2*, float2*, int64_t, const float2*, const float2*, float);
+
+template <int L> struct RowGeom {
+    static constexpr int T = Sched<L>::T;
+    static constexpr int B = T >= 256 ? 1 : 256 / T;  // records per CTA
+    static constexpr int THREADS = B * T;
+    static constexpr size_t SMEM = Sched<L>::NPASS > 1 ? sizeof(float2) * B * L : 0;
+};
+template <int L> struct FsGeom {
+    static constexpr int COLS = L >= 2048 ? 8 : 16;   // tile width (columns or rows)
+    static constexpr int THREADS = COLS * Sched<L>::T;
+    static constexpr size_t SMEM = sizeof(float2) * COLS * L;
+};
+
+struct KernelSet {
+    const void* fn = nullptr;
+    int threads = 0;
+    size_t smem = 0;
+    int cols = 0;
+};
+
+template <int L> static KernelSet row_kernel(bool inv) {
+    KernelSet k;
+    k.fn = inv ? (const void*)&k_rows<L, RowGeom<L>::B, true> : (const void*)&k_rows<L, RowGeom<L>::B, false>;
+    k.threads = RowGeom<L>::THREADS;
+    k.smem = RowGeom<L>::SMEM;
+    k.cols = RowGeom<L>::B;
+    return k;
+}
+template <int L> static KernelSet fs_col_kernel(int n2, bool inv) {
+    constexpr int C = FsGeom<L>::COLS;
+    KernelSet k;
+    k.fn = inv ? (const void*)&k_fs_cols<L, C, true> : (const void*)&k_fs_cols<L, C, false>;
+    k.threads = FsGeom<L>::THREADS;
+    k.smem = Sched<L>::NPASS > 1 ? FsGeom<L>::SMEM : 0;
+    k.cols = C;
+    (void)n2;
+    return k;
+}
+template <int L> static KernelSet fs_row_kernel(bool inv) {
+    constexpr int C = FsGeom<L>::COLS;
+    KernelSet k;
+    k.fn = inv ? (const void*)&k_fs_rows<L, C, true> : (const void*)&k_fs_rows<L, C, false>;
+    k.threads = FsGeom<L>::THREADS;
+    k.smem = FsGeom<L>::SMEM;  // the transposing tile load always uses shared memory
+    k.cols = C;
+    return k;
+}
+
+#define BFFT_L_CASES(M) \
+    M(1, 2) M(2, 4) M(3, 8) M(4, 16) M(5, 32) M(6, 64) M(7, 128) M(8, 256) M(9, 512) M(10, 1024) \
+    M(11, 2048)
+
+static KernelSet pick_row(int log2l, bool inv) {
+    switch (log2l) {
+#define M(k, L) case k: return row_kernel<L>(inv);
+        BFFT_L_CASES(M)
+#undef M
+        case 12: return row_kernel<4096>(inv);
+        case 13: return row_kernel<8192>(inv);
+        case 14: return row_kernel<16384>(inv);
+        default: return KernelSet{};
+    }
+}
+static KernelSet pick_fs_col(int log2l, int n2, bool inv) {
+    switch (log2l) {
+#define M(k, L) case k: return fs_col_kernel<L>(n2, inv);
+        BFFT_L_CASES(M)
+#undef M
+        default: return KernelSet{};
+    }
+}
+static KernelSet pick_fs_row(int log2l, bool inv) {
+    switch (log2l) {
+#define M(k, L) case k: return fs_row_kernel<L>(inv);
+        BFFT_L_CASES(M)
+#undef M
+        default: return KernelSet{};
+    }
+}
+
+struct ClusterChoice {
+    int n1 = 0, n2 = 0, c = 0;
+    KernelSet k;
+};
+template <int N1, int N2, int C> static ClusterChoice cluster_kernel(bool inv) {
+    using CF = ClusterCfg<N1, N2, C>;
+    ClusterChoice ch;
+    ch.n1 = N1;
+    ch.n2 = N2;
+    ch.c = C;
+    ch.k.fn = inv ? (const void*)&k_cluster<N1, N2, C, true> : (const void*)&k_cluster<N1, N2, C, false>;
+    ch.k.threads = CF::NT;
+    ch.k.smem = CF::SMEM;
+    return ch;
+}
+// Cluster configurations: N = N1*N2 over C CTAs.
+static ClusterChoice pick_cluster(int log2n, int want_c, bool inv) {
+    switch (log2n) {
+        case 13: return cluster_kernel<64, 128, 4>(inv);
+        case 14: return cluster_kernel<128, 128, 4>(inv);
+        case 15: return cluster_kernel<128, 256, 8>(inv);
+        case 16:
+            if (want_c == 16) return cluster_kernel<256, 256, 16>(inv);
+            return cluster_kernel<256, 256, 8>(inv);
+        case 17: return cluster_kernel<512, 256, 16>(inv);
+        default: return ClusterChoice{};
+    }
+}
+
+// ------------------------------------------------------------ twiddle tables
+// Stockham per-pass table for length L (same schedule as Sched<L>): for each
+// pass p >= 1 with sub-length Ns, entries [(q-1)*Ns + jj] = W_{16 Ns}^{jj q},
+// computed in fp64 and rounded once to fp32.
+static void stockham_table(int L, std::vector<float2>& out) {
+    out.clear();
+    if (L <= 16) return;
+    const int K = ilog2(L);
+    const int R0 = (K & 3) ? (1 << (K & 3)) : 16;
+    const int npass = (K & 3) ? 1 + K / 4 : K / 4;
+    for (int p = 1; p < npass; ++p) {
+        const int Ns = R0 * (1 << (4 * (p - 1)));
+        const int M = 16 * Ns;
+        for (int q = 1; q < 16; ++q)
+            for (int jj = 0; jj < Ns; ++jj) {
+                const long long m = (long long)jj * q;  // < M
+                const double ang = -2.0 * M_PI * (double)m / (double)M;
+                out.push_back(make_float2((float)cos(ang), (float)sin(ang)));
+            }
+    }
+}
+
+// ------------------------------------------------------------ the plan
+struct fft_plan {
+    int64_t n = 0, batch = 0;
+    int dir = 0, variant = 0, device = 0, log2n = 0, sms = 0;
+    int n1 = 0, n2 = 0, cluster = 1;
+    float scale = 1.f;
+    float2* d_tab = nullptr;          // all twiddle tables
+    size_t tab_bytes = 0;
+    const float2* tw_a = nullptr;     // table for the first (or only) length
+    const float2* tw_b = nullptr;     // table for the second length
+    float2* d_scratch = nullptr;      // four-step wave scratch
+    int64_t wave = 0;                 // records per four-step wave
+    KernelSet ka, kb;                 // kernels (kb only for four-step)
+    int grid_a = 0, grid_b = 0;       // persistent/capped grid sizes (per full batch)
+    int occ_a = 0, occ_b = 0;
+};
+
+static int validate(int64_t n, int64_t batch, int dir) {
+    if (n < 2 || n > (1 << 22) || (n & (n - 1)) != 0)
+        return bfft_set_error(FFT_E_SIZE, "unsupported transform size: %lld", (long long)n);
+    if (batch < 1) return bfft_set_error(FFT_E_BATCH, "batch must be >= 1: %lld", (long long)batch);
+    if (dir != FFT_FORWARD && dir != FFT_INVERSE && dir != 0)
+        return bfft_set_error(FFT_E_DIR, "direction must be -1 or +1: %d", dir);
+    return FFT_OK;
+}
+
+static int default_variant(int log2n) {
+    if (const char* e = getenv("BLOCKFFT_VARIANT")) {
+        int v = atoi(e);
+        if (v >= 1 && v <= 3) return v;
+    }
+    if (log2n <= 12) return FFT_VARIANT_SINGLE;
+    if (log2n <= 17) return FFT_VARIANT_CLUSTER;
+    return FFT_VARIANT_FOURSTEP;
+}
+
+static int set_smem(const KernelSet& k) {
+    if (k.smem > 48 * 1024)
+        CUDA_TRY(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
+    return FFT_OK;
+}
+
+static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant) {
+    int rc = validate(n, batch, dir);
+    if (rc) return rc;
+    if (dir == 0 && variant != FFT_VARIANT_IDENTITY && variant != FFT_VARIANT_AUTO)
+        return bfft_set_error(FFT_E_DIR, "direction 0 (identity) needs the identity variant: %d", variant);
+    if (dir != 0 && variant == FFT_VARIANT_IDENTITY)
+        return bfft_set_error(FFT_E_DIR, "identity variant takes direction 0: %d", dir);
+    if (variant < 0 || variant > FFT_VARIANT_IDENTITY)
+        return bfft_set_error(FFT_E_ARG, "unknown variant: %d", variant);
+    p->n = n;
+    p->batch = batch;
+    p->dir = dir;
+    p->log2n = ilog2((int)n);
+    p->scale = 1.0f / (float)n;
+    CUDA_TRY(cudaGetDevice(&p->device));
+    CUDA_TRY(cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, p->device));
+    const bool inv = dir == FFT_INVERSE;
+    if (dir == 0) variant = FFT_VARIANT_IDENTITY;
+    if (variant == FFT_VARIANT_AUTO) variant = default_variant(p->log2n);
+    p->variant = variant;
+
+    std::vector<float2> ta, tb;
+    if (variant == FFT_VARIANT_IDENTITY) {
+        p->n1 = (int)n;
+        p->n2 = 1;
+    } else if (variant == FFT_VARIANT_SINGLE) {
+        if (p->log2n > 14) return bfft_set_error(FFT_E_SIZE, "unsupported transform size for single-pass variant: %lld", (long long)n);
+        p->ka = pick_row(p->log2n, inv);
+        p->n1 = (int)n;
+        p->n2 = 1;
+        stockham_table((int)n, ta);
+    } else if (variant == FFT_VARIANT_CLUSTER) {
+        int want = 8;
+        if (const char* e = getenv("BLOCKFFT_CLUSTER_SIZE")) want = atoi(e);
+        ClusterChoice ch = pick_cluster(p->log2n, want, inv);
+        if (!ch.k.fn) return bfft_set_error(FFT_E_SIZE, "unsupported transform size for cluster variant: %lld", (long long)n);
+        p->ka = ch.k;
+        p->n1 = ch.n1;
+        p->n2 = ch.n2;
+        p->cluster = ch.c;
+        stockham_table(ch.n1, ta);
+        stockham_table(ch.n2, tb);
+    } else if (variant == FFT_VARIANT_FOURSTEP) {
+        if (p->log2n < 2) return bfft_set_error(FFT_E_SIZE, "unsupported transform size for four-step variant: %lld", (long long)n);
+        const int k1 = p->log2n / 2, k2 = p->log2n - k1;
+        p->n1 = 1 << k1;
+        p->n2 = 1 << k2;
+        p->ka = pick_fs_col(k1, p->n2, inv);
+        p->kb = pick_fs_row(k2, inv);
+        if (p->ka.cols > p->n2) p->ka = KernelSet{};
+        if (p->kb.cols > p->n1) p->kb = KernelSet{};
+        if (!p->ka.fn || !p->kb.fn)
+            return bfft_set_error(FFT_E_SIZE, "unsupported transform size for four-step variant: %lld", (long long)n);
+        stockham_table(p->n1, ta);
+        stockham_table(p->n2, tb);
+    } else {
+        return bfft_set_error(FFT_E_ARG, "unknown variant: %d", variant);
+    }
+
+    // upload tables (one allocation; b after a, 256-byte aligned)
+    const size_t a_bytes = ta.size() * sizeof(float2);
+    const size_t b_off = (a_bytes + 255) & ~(size_t)255;
+    const size_t tot = b_off + tb.size() * sizeof(float2);
+    if (tot > 0) {
+        cudaError_t e = cudaMalloc(&p->d_tab, tot);
+        if (e != cudaSuccess) return bfft_set_error(FFT_E_NOMEM, "cudaMalloc(%zu) for twiddle tables failed: %s", tot, cudaGetErrorString(e));
+        if (a_bytes) CUDA_TRY(cudaMemcpy(p->d_tab, ta.data(), a_bytes, cudaMemcpyHostToDevice));
+        if (!tb.empty()) CUDA_TRY(cudaMemcpy((char*)p->d_tab + b_off, tb.data(), tb.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    }
+    p->tab_bytes = tot;
+    p->tw_a = p->d_tab;
+    p->tw_b = (const float2*)((const char*)p->d_tab + b_off);
+
+    // launch geometry
+    if (variant == FFT_VARIANT_SINGLE) {
+        rc = set_smem(p->ka);
+        if (rc) return rc;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ_a, p->ka.fn, p->ka.threads, p->ka.smem));
+        p->occ_a = std::max(p->occ_a, 1);
+    } else if (variant == FFT_VARIANT_CLUSTER) {
+        rc = set_smem(p->ka);
+        if (rc) return rc;
+        if (p->cluster > 8)
+            CUDA_TRY(cudaFuncSetAttribute(p->ka.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = p->cluster;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(p->cluster * p->sms, 1, 1);
+        cfg.blockDim = dim3(p->ka.threads, 1, 1);
+        cfg.dynamicSmemBytes = p->ka.smem;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveClusters(&ncl, p->ka.fn, &cfg));
+        if (ncl < 1) return bfft_set_error(FFT_E_CUDA, "cluster of %d CTAs x %zu B shared memory cannot be scheduled", p->cluster, p->ka.smem);
+        p->occ_a = ncl;  // co-resident clusters
+    } else if (variant == FFT_VARIANT_FOURSTEP) {
+        rc = set_smem(p->ka);
+        if (rc) return rc;
+        rc = set_smem(p->kb);
+        if (rc) return rc;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ_a, p->ka.fn, p->ka.threads, p->ka.smem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ_b, p->kb.fn, p->kb.threads, p->kb.smem));
+        p->occ_a = std::max(p->occ_a, 1);
+        p->occ_b = std::max(p->occ_b, 1);
+        int64_t wave_bytes = 256ll << 20;
+        if (const char* e = getenv("BLOCKFFT_FS_WAVE_BYTES")) wave_bytes = std::max(1ll, atoll(e));
+        p->wave = std::max<int64_t>(1, std::min<int64_t>(batch, wave_bytes / (8 * n)));
+        const size_t sb = (size_t)p->wave * (size_t)n * sizeof(float2);
+        cudaError_t e = cudaMalloc(&p->d_scratch, sb);
+        if (e != cudaSuccess) return bfft_set_error(FFT_E_NOMEM, "cudaMalloc(%zu) for four-step scratch failed: %s", sb, cudaGetErrorString(e));
+    }
+    return FFT_OK;
+}
+
+static void plan_free(fft_plan* p) {
+    if (!p) return;
+    if (p->d_tab) cudaFree(p->d_tab);
+    if (p->d_scratch) cudaFree(p->d_scratch);
+    delete p;
+}
+
+extern "C" fft_plan* fft_plan_create_ex(int64_t n, int64_t batch, int dir, int variant) {
+    bfft_clear_error();
+    fft_plan* p = new (std::nothrow) fft_plan();
+    if (!p) {
+        bfft_set_error(FFT_E_NOMEM, "out of host memory");
+        return nullptr;
+    }
+    if (plan_init(p, n, batch, dir, variant) != FFT_OK) {
+        std::string keep = g_err;
+        int code = g_code;
+        plan_free(p);
+        g_err = keep;
+        g_code = code;
+        return nullptr;
+    }
+    return p;
+}
+
+extern "C" fft_plan* fft_plan_create(int64_t n, int64_t batch, int dir) {
+    return fft_plan_create_ex(n, batch, dir, FFT_VARIANT_AUTO);
+}
+
+extern "C" void fft_plan_destroy(fft_plan* p) { plan_free(p); }
+
+extern "C" int fft_plan_get_info(const fft_plan* p, fft_plan_info* info) {
+    if (!p || !info) return bfft_set_error(FFT_E_ARG, "null plan or info pointer");
+    info->n = p->n;
+    info->batch = p->batch;
+    info->dir = p->dir;
+    info->variant = p->variant;
+    info->device = p->device;
+    info->n1 = p->n1;
+    info->n2 = p->n2;
+    info->cluster = p->cluster;
+    info->scratch_bytes = p->d_scratch ? p->wave * p->n * 8 : 0;
+    info->table_bytes = (int64_t)p->tab_bytes;
+    if (p->variant == FFT_VARIANT_FOURSTEP)
+        info->kernels_per_exec = (int)(2 * ((p->batch + p->wave - 1) / p->wave));
+    else
+        info->kernels_per_exec = 1;
+    return FFT_OK;
+}
+
+// ------------------------------------------------------------ exec
+static int launch(const fft_plan* p, const float2* in, float2* out, int64_t count, cudaStream_t st) {
+    const int64_t n = p->n;
+    switch (p->variant) {
+        case FFT_VARIANT_IDENTITY: {
+            const int64_t n16 = count * n * 8 / 16;
+            const int threads = 256;
+            const int64_t want = (n16 + threads - 1) / threads;
+            const int grid = (int)std::min<int64_t>(want, (int64_t)p->sms * 16);
+            k_copy<<<grid, threads, 0, st>>>((const float4*)in, (float4*)out, n16);
+            break;
+        }
+        case FFT_VARIANT_SINGLE: {
+            const int64_t groups = (count + p->ka.cols - 1) / p->ka.cols;
+            const int grid = (int)std::min<int64_t>(groups, (int64_t)p->sms * p->occ_a * 8);
+            auto fn = (RowFn)p->ka.fn;
+            fn<<<grid, p->ka.threads, p->ka.smem, st>>>(in, out, count, p->tw_a, p->scale);
+            break;
+        }
+        case FFT_VARIANT_CLUSTER: {
+            const int64_t ncl = std::min<int64_t>(count, p->occ_a);
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = p->cluster;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3((unsigned)(ncl * p->cluster), 1, 1);
+            cfg.blockDim = dim3(p->ka.threads, 1, 1);
+            cfg.dynamicSmemBytes = p->ka.smem;
+            cfg.stream = st;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            CUDA_TRY(cudaLaunchKernelEx(&cfg, (ClusterFn)p->ka.fn, in, out, count, p->tw_a, p->tw_b, p->scale));
+            break;
+        }
+        case FFT_VARIANT_FOURSTEP: {
+            const int k1 = ilog2(p->n1), k2 = ilog2(p->n2);
+            for (int64_t r0 = 0; r0 < count; r0 += p->wave) {
+                const int64_t w = std::min<int64_t>(p->wave, count - r0);
+                const int64_t ta = w * (p->n2 / p->ka.cols), tb = w * (p->n1 / p->kb.cols);
+                const int ga = (int)std::min<int64_t>(ta, (int64_t)p->sms * p->occ_a * 8);
+                const int gb = (int)std::min<int64_t>(tb, (int64_t)p->sms * p->occ_b * 8);
+                ((ColFn)p->ka.fn)<<<ga, p->ka.threads, p->ka.smem, st>>>(in + r0 * n, p->d_scratch, w, k2, p->tw_a);
+                ((RowTFn)p->kb.fn)<<<gb, p->kb.threads, p->kb.smem, st>>>(p->d_scratch, out + r0 * n, w, k1, p->tw_b, p->scale);
+            }
+            break;
+        }
+        default:
+            return bfft_set_error(FFT_E_ARG, "plan has unknown variant %d", p->variant);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return bfft_set_error(FFT_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return FFT_OK;
+}
+
+extern "C" int fft_exec_range(const fft_plan* p, const void* in, void* out, int64_t count, void* stream) {
+    bfft_clear_error();
+    if (!p) return bfft_set_error(FFT_E_ARG, "null plan");
+    if (!in || !out) return bfft_set_error(FFT_E_ARG, "null data pointer");
+    if (((uintptr_t)in & 15) || ((uintptr_t)out & 15))
+        return bfft_set_error(FFT_E_ARG, "data pointers must be 16-byte aligned: in=%p out=%p", in, out);
+    if (count < 1 || count > p->batch)
+        return bfft_set_error(FFT_E_ARG, "record count out of range: expected 1..%lld, got %lld", (long long)p->batch, (long long)count);
+    const uintptr_t bytes = (uintptr_t)(count * p->n * 8);
+    const uintptr_t a = (uintptr_t)in, b = (uintptr_t)out;
+    if (a != b && a < b + bytes && b < a + bytes)
+        return bfft_set_error(FFT_E_ARG, "input and output partially overlap");
+    int dev = -1;
+    CUDA_TRY(cudaGetDevice(&dev));
+    if (dev != p->device)
+        return bfft_set_error(FFT_E_DEVICE, "plan belongs to device %d, current device is %d", p->device, dev);
+    return launch(p, (const float2*)in, (float2*)out, count, (cudaStream_t)stream);
+}
+
+extern "C" int fft_exec(const fft_plan* p, const void* in, void* out, void* stream) {
+    if (!p) return bfft_set_error(FFT_E_ARG, "null plan");
+    return fft_exec_range(p, in, out, p->batch, stream);
+}
+
+// ------------------------------------------------------------ partitioner
+extern "C" int64_t fft_file_records(int64_t file_bytes, int64_t record_len) {
+    bfft_clear_error();
+    int rc = validate(record_len, 1, FFT_FORWARD);
+    if (rc) return -rc;
+    if (file_bytes < 0 || file_bytes % 8)
+        return -bfft_set_error(FFT_E_ARG, "file size %lld is not a multiple of 8 bytes", (long long)file_bytes);
+    if (file_bytes == 0) return -bfft_set_error(FFT_E_EMPTY, "empty input");
+    const int64_t rb = 8 * record_len;
+    return (file_bytes + rb - 1) / rb;
+}
+
+extern "C" int fft_partition(int64_t total, int nparts, int part, int64_t* first, int64_t* count) {
+    bfft_clear_error();
+    if (!first || !count || total < 0 || nparts < 1 || part < 0 || part >= nparts)
+        return bfft_set_error(FFT_E_ARG, "invalid partition request: total=%lld nparts=%d part=%d",
+                              (long long)total, nparts, part);
+    // floor(part*R/G) without overflow for R up to 2^62: split R = qG + rem.
+    auto bound = [&](int64_t g) {
+        const int64_t q = total / nparts, rem = total % nparts;
+        return q * g + (rem * g) / nparts;
+    };
+    *first = bound(part);
+    *count = bound(part + 1) - *first;
+    return FFT_OK;
+}

@@ -1,0 +1,150 @@
+"""GPU tests of the file pipeline (fft_file: partition -> stream -> write by
+offset) and the host streamer (fft_exec_host) against the oracle, plus the
+identity-kernel byte-exact round trip and the
+SPEC error conventions."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+bf = pytest.importorskip("paper_1407_6915_b200")
+
+
+def write_file(path, samples):
+    np.asarray(samples, dtype="<c8").tofile(path)
+    return os.path.getsize(path)
+
+
+def read_c64(path, n):
+    return np.fromfile(path, dtype="<c8").reshape(-1, n)
+
+
+def test_config1_file_forward(tmp_path):
+    # BASELINE.json configs[0]: 16 records x 1024-point complex64 forward FFT
+    # from a synthetic seeded file.
+    n, r = 1024, 16
+    src, dst = tmp_path / "in.c64", tmp_path / "out.c64"
+    write_file(src, synth.random_samples(synth.DEFAULT_SEED, 0, n * r))
+    st = bf.fft_file(str(src), str(dst), n, 1)
+    assert st["records"] == r and st["bytes_in"] == r * 8 * n
+    y = read_c64(dst, n)
+    ref = oracle.file_transform(src.read_bytes(), n)
+    assert np.all(oracle.rel_l2(y, ref) <= oracle.tolerance(n))
+    assert not os.path.exists(str(dst) + ".tmp")
+
+
+def test_tail_padding_and_output_size(tmp_path):
+    n = 1024
+    s = synth.random_samples(3, 0, 5 * n + 100)
+    src, dst = tmp_path / "in.c64", tmp_path / "out.c64"
+    write_file(src, s)
+    bf.fft_file(str(src), str(dst), n, 1)
+    assert os.path.getsize(dst) == 6 * 8 * n           # R*8N, final record zero-padded
+    y = read_c64(dst, n)
+    ref = oracle.file_transform(src.read_bytes(), n)
+    assert np.all(oracle.rel_l2(y, ref) <= oracle.tolerance(n))
+
+
+@pytest.mark.parametrize("n", [256, 1 << 16])
+def test_identity_byte_exact(tmp_path, n):
+    src, dst = tmp_path / "in.c64", tmp_path / "out.c64"
+    write_file(src, synth.random_samples(11, 0, 37 * n))
+    bf.fft_file(str(src), str(dst), n, 1, direction=bf.FFT_IDENTITY, chunk_bytes=8 * n * 5)
+    assert src.read_bytes() == dst.read_bytes()
+
+
+@pytest.mark.parametrize("n,variant", [(1024, 0), (1 << 16, 0), (1 << 18, 0), (1 << 16, 3)])
+def test_chunking_and_streaming_bit_identical_to_in_hbm(tmp_path, n, variant):
+    # results depend only on (N, dir): not on chunk size, GPU count or path
+    r = 23
+    s = synth.random_samples(21, 0, r * n)
+    src = tmp_path / "in.c64"
+    write_file(src, s)
+    outs = []
+    for cb in (8 * n * 4, 8 * n * 7, 0):
+        dst = tmp_path / f"out_{cb}.c64"
+        bf.fft_file(str(src), str(dst), n, 1, chunk_bytes=cb, variant=variant)
+        outs.append(read_c64(dst, n))
+    x = torch.from_numpy(s.reshape(r, n)).cuda()
+    y = torch.empty_like(x)
+    with bf.Plan(n, r, bf.FFT_FORWARD, variant) as p:
+        p.exec(x, y)
+    torch.cuda.synchronize()
+    y = y.cpu().numpy()
+    for o in outs:
+        assert np.array_equal(o, y)
+    ng = torch.cuda.device_count()
+    if ng > 1:
+        dst = tmp_path / "out_multi.c64"
+        bf.fft_file(str(src), str(dst), n, ng, chunk_bytes=8 * n * 3, variant=variant)
+        assert np.array_equal(read_c64(dst, n), y)
+
+
+def test_forward_then_inverse_pipeline(tmp_path):
+    # forward pipeline then inverse pipeline -> <= 1e-5 vs original
+    n = 4096
+    s = synth.random_samples(8, 0, 9 * n)
+    a, b, c = tmp_path / "a", tmp_path / "b", tmp_path / "c"
+    write_file(a, s)
+    bf.fft_file(str(a), str(b), n, 1, direction=bf.FFT_FORWARD)
+    bf.fft_file(str(b), str(c), n, 1, direction=bf.FFT_INVERSE)
+    e = oracle.rel_l2(read_c64(c, n), s.reshape(-1, n))
+    assert np.all(e <= 1e-5)
+
+
+def test_sine3_spectral_check(tmp_path):
+    # SPEC.md:469 / :515: sine:3 records -> peaks at bins 3 and N-3 of N/2 +- 1%,
+    # off-peak energy < 1% of total, for every record.
+    n, r = 1024, 8
+    rec = synth.record("tone", n, 3)
+    src, dst = tmp_path / "in", tmp_path / "out"
+    write_file(src, np.tile(rec, r))
+    bf.fft_file(str(src), str(dst), n, 1)
+    mag = np.abs(read_c64(dst, n))
+    assert np.all(np.abs(mag[:, [3, n - 3]] - n / 2) <= 0.01 * n / 2)
+    off = np.delete(mag, [3, n - 3], axis=1)
+    assert np.all((off ** 2).sum(1) < 0.01 * (mag ** 2).sum(1))
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_exec_host_matches_device(pinned):
+    n, r = 1 << 16, 37
+    s = torch.from_numpy(synth.random_records(4, n, 0, r))
+    h = s.pin_memory() if pinned else s.clone()
+    out = torch.empty_like(h).pin_memory() if pinned else torch.empty_like(h)
+    st = bf.exec_host(h, n, bf.FFT_FORWARD, 0, out=out, chunk_bytes=8 * n * 8)
+    assert st["records"] == r and st["chunks"] == 5
+    x = s.cuda()
+    with bf.Plan(n, r) as p:
+        y = p.exec(x, torch.empty_like(x))
+    torch.cuda.synchronize()
+    assert torch.equal(out, y.cpu())
+    assert torch.equal(h, s)      # out-of-place: input untouched
+
+
+def test_file_errors(tmp_path):
+    out = tmp_path / "out"
+    with pytest.raises(bf.FFTError) as ei:
+        bf.fft_file(str(tmp_path / "missing"), str(out), 1024, 1)
+    assert ei.value.code == 8
+    bad = tmp_path / "bad"
+    bad.write_bytes(b"\0" * 12)
+    with pytest.raises(bf.FFTError) as ei:
+        bf.fft_file(str(bad), str(out), 1024, 1)
+    assert ei.value.code == 4
+    empty = tmp_path / "empty"
+    empty.write_bytes(b"")
+    with pytest.raises(bf.FFTError) as ei:
+        bf.fft_file(str(empty), str(out), 1024, 1)
+    assert ei.value.code == 9
+    good = tmp_path / "good"
+    write_file(good, np.zeros(2048, np.complex64))
+    with pytest.raises(bf.FFTError) as ei:
+        bf.fft_file(str(good), str(out), 1024, 99)
+    assert ei.value.code == 5
+    assert not out.exists() and not os.path.exists(str(out) + ".tmp")
