@@ -61,7 +61,7 @@ enum fft_variant {
     FFT_VARIANT_CLUSTER = 2,  /* one kernel, record across a CTA cluster
                                  exchanging through DSMEM, 2^10 <= N <= 2^17   */
     FFT_VARIANT_FOURSTEP = 3, /* two kernels (column FFT + twiddle, row FFT +
-                                 transposed store) through HBM scratch, N >= 4 */
+                                 transposed store) through HBM scratch, N >= 256 */
     FFT_VARIANT_IDENTITY = 4  /* copy kernel: out = in bit-exactly (pipeline
                                  test mode)                      */
 };
@@ -120,6 +120,8 @@ typedef struct fft_plan_info {
     int cluster;          /* CTAs per cluster (cluster variant), else 1        */
     int64_t scratch_bytes;/* HBM scratch owned by the plan                     */
     int64_t table_bytes;  /* device twiddle tables owned by the plan           */
+    int resident;         /* co-resident clusters (cluster variant) or CTAs per
+                             SM of the first kernel (other variants)          */
 } fft_plan_info;
 
 /* Fill *info for a plan.  Returns FFT_OK or FFT_E_ARG.                       */

@@ -35,7 +35,7 @@ class PlanInfo(ctypes.Structure):
                 ("variant", ctypes.c_int), ("kernels_per_exec", ctypes.c_int),
                 ("device", ctypes.c_int), ("n1", ctypes.c_int64), ("n2", ctypes.c_int64),
                 ("cluster", ctypes.c_int), ("scratch_bytes", ctypes.c_int64),
-                ("table_bytes", ctypes.c_int64)]
+                ("table_bytes", ctypes.c_int64), ("resident", ctypes.c_int)]
 
 
 class StreamOpts(ctypes.Structure):

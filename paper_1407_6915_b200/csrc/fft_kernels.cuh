@@ -211,132 +211,6 @@ k_fs_rows(const float2* __restrict__ y, float2* __restrict__ out, int64_t nrec, 
     }
 }
 
-// ======================================================================
-// Cluster variant.  A cluster of C CTAs owns one record at a time
-// (persistent over records).  CTA `rank` computes phase A for columns
-// n2 in [rank*CA, (rank+1)*CA) (CA = N2/C) and pushes Y[k1][n2] straight
-// into the shared memory of CTA k1 / CB (CB = N1/C), which then computes
-// phase B for rows k1 in its range and stores X[k1 + N1 k2].
-// ======================================================================
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ uint32_t map_rank(uint32_t addr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void st_cluster(uint32_t addr, float2 v) {
-    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
-}
-__device__ __forceinline__ void cluster_arrive() {
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() {
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t cluster_id_x() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t ncluster_x() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
-    return r;
-}
-
-template <int N1, int N2, int C>
-struct ClusterCfg {
-    static constexpr int N = N1 * N2;
-    static constexpr int CA = N2 / C;   // phase-A columns per CTA
-    static constexpr int CB = N1 / C;   // phase-B columns (rows k1) per CTA
-    static constexpr int NT = N / (16 * C);
-    static constexpr int TA = Sched<N1>::T, TB = Sched<N2>::T;
-    static_assert(Sched<N1>::P == 16 && Sched<N2>::P == 16, "cluster variant needs N1, N2 >= 16");
-    static_assert(CA * TA == NT && CB * TB == NT, "thread mapping");
-    static_assert(CA >= 16 && CB >= 16, "column tiles of >= 16 keep shared accesses conflict-free");
-    static constexpr size_t SMEM = 2 * sizeof(float2) * (N / C);  // work + recv
-};
-
-template <int N1, int N2, int C, bool INV>
-__global__ void __launch_bounds__(ClusterCfg<N1, N2, C>::NT)
-k_cluster(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
-          const float2* __restrict__ tw1, const float2* __restrict__ tw2, float scale) {
-    using CF = ClusterCfg<N1, N2, C>;
-    constexpr int N = CF::N, CA = CF::CA, CB = CF::CB, TA = CF::TA, TB = CF::TB;
-    extern __shared__ float2 sm[];
-    float2* work = sm;             // phase-A exchange buffer, N/C entries
-    float2* recv = sm + N / C;     // phase-B input (written by all ranks) and exchange
-    const int tid = threadIdx.x;
-    const uint32_t rank = cluster_rank();
-    const int64_t cid = cluster_id_x(), ncl = ncluster_x();
-
-    // phase-A mapping: column n2, butterfly row tA
-    const int colA = tid % CA, tA = tid / CA;
-    const int n2 = (int)rank * CA + colA;
-    // phase-B mapping: column k1 (local kb), butterfly row tB
-    const int colB = tid % CB, tB = tid / CB;
-    const int k1b = (int)rank * CB + colB;
-
-    // W_N^{n2 k1} for this thread's k1 = tA + q*TA: fixed for the whole kernel.
-    float2 w4[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q)
-        w4[q] = twiddle_exact(((uint32_t)n2 * (uint32_t)(tA + q * TA)) & (N - 1), N);
-
-    // Remote base of every destination's recv buffer, and this thread's
-    // destination offsets: Y[k1][n2] -> rank k1/CB, recv[ColLayout<CB>(n2, k1 % CB)].
-    const uint32_t recv_local = smem_addr(recv);
-    uint32_t dst_addr[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        const int k1 = tA + q * TA;
-        const uint32_t dst_rank = (uint32_t)(k1 / CB);
-        dst_addr[q] = map_rank(recv_local, dst_rank) +
-                      (uint32_t)(ColLayout<CB>::at(n2, k1 % CB) * sizeof(float2));
-    }
-    const TableTw<N1> tabA{tw1};
-    const TableTw<N2> tabB{tw2};
-    auto addrA = [&](int e) { return ColLayout<CA>::at(e, colA); };
-    auto addrB = [&](int e) { return ColLayout<CB>::at(e, colB); };
-
-    cluster_arrive();  // "recv is free" for the first record
-    for (int64_t r = cid; r < nrec; r += ncl) {
-        // ---- phase A: column FFTs of length N1 over n1, times W_N^{n2 k1}
-        const float2* src = in + r * N + n2 + (int64_t)tA * N2;
-        float2 v[16];
-#pragma unroll
-        for (int s = 0; s < 16; ++s) {
-            float2 x = ld_stream(src + s * TA * N2);
-            v[s] = INV ? conjf2(x) : x;
-        }
-        fft_engine<N1>(v, tA, work, addrA, tabA);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = cmul(v[q], w4[q]);
-        // ---- exchange: all-to-all through distributed shared memory
-        cluster_wait();    // every rank finished reading its recv for record r - ncl
-#pragma unroll
-        for (int q = 0; q < 16; ++q) st_cluster(dst_addr[q], v[q]);
-        cluster_arrive();
-        cluster_wait();    // all pushes for record r have landed
-        // ---- phase B: row FFTs of length N2 over n2, stored to X[k1 + N1 k2]
-#pragma unroll
-        for (int s = 0; s < 16; ++s) v[s] = recv[addrB(tB + s * TB)];
-        fft_engine<N2>(v, tB, recv, addrB, tabB);
-        cluster_arrive();  // this thread is done with recv
-        float2* dst = out + r * N + k1b + (int64_t)tB * N1;
-#pragma unroll
-        for (int q = 0; q < 16; ++q)
-            st_stream(dst + (int64_t)q * TB * N1, INV ? scale_conj(v[q], scale) : v[q]);
-    }
-    cluster_wait();
-}
 
 // ======================================================================
 // Identity kernel: out = in, bit-exact, 16-byte vectors.

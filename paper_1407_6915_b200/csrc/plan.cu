@@ -18,6 +18,10 @@
 
 #include "../../include/blockfft.h"
 #include "common.h"
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "fft_cluster.cuh"
 #include "fft_kernels.cuh"
 
 using namespace bfft;
@@ -57,7 +61,7 @@ extern "C" int fft_version(void) { return BLOCKFFT_VERSION; }
 using RowFn = void (*)(const float2*, float2*, int64_t, const float2*, float);
 using ColFn = void (*)(const float2*, float2*, int64_t, int, const float2*);
 using RowTFn = void (*)(const float2*, float2*, int64_t, int, const float2*, float);
-using ClusterFn = void (*)(const float2*, float2*, int64_t, const float2*, const float2*, float);
+using ClusterFn = void (*)(const CUtensorMap, float2*, int64_t, const float2*, const float2*, float);
 
 template <int L> struct RowGeom {
     static constexpr int T = Sched<L>::T;
@@ -142,13 +146,20 @@ struct ClusterChoice {
     int n1 = 0, n2 = 0, c = 0;
     KernelSet k;
 };
+static int cluster_xch() {
+    const char* e = getenv("BLOCKFFT_CLUSTER_XCH");
+    return e ? atoi(e) : XCH_STAS;
+}
 template <int N1, int N2, int C> static ClusterChoice cluster_kernel(bool inv) {
     using CF = ClusterCfg<N1, N2, C>;
     ClusterChoice ch;
     ch.n1 = N1;
     ch.n2 = N2;
     ch.c = C;
-    ch.k.fn = inv ? (const void*)&k_cluster<N1, N2, C, true> : (const void*)&k_cluster<N1, N2, C, false>;
+    if (cluster_xch() == XCH_BULK)
+        ch.k.fn = inv ? (const void*)&k_cluster<N1, N2, C, true, XCH_BULK> : (const void*)&k_cluster<N1, N2, C, false, XCH_BULK>;
+    else
+        ch.k.fn = inv ? (const void*)&k_cluster<N1, N2, C, true, XCH_STAS> : (const void*)&k_cluster<N1, N2, C, false, XCH_STAS>;
     ch.k.threads = CF::NT;
     ch.k.smem = CF::SMEM;
     return ch;
@@ -162,9 +173,44 @@ static ClusterChoice pick_cluster(int log2n, int want_c, bool inv) {
         case 16:
             if (want_c == 16) return cluster_kernel<256, 256, 16>(inv);
             return cluster_kernel<256, 256, 8>(inv);
-        case 17: return cluster_kernel<512, 256, 16>(inv);
+        case 17: return cluster_kernel<256, 512, 16>(inv);
         default: return ClusterChoice{};
     }
+}
+
+// ------------------------------------------------------------ TMA tensor maps
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+        else
+            cudaGetLastError();
+    }
+    return fn;
+}
+
+// Records viewed as a 3-D tensor of 8-byte elements [count][n1][n2] (n2
+// fastest); box = {box_cols, box_rows, 1}: one record's column tile.
+static int make_record_tmap(CUtensorMap* m, const void* base, int64_t count, int n1, int n2, int box_cols,
+                            int box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return bfft_set_error(FFT_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    cuuint64_t dims[3] = {(cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)count};
+    cuuint64_t strides[2] = {(cuuint64_t)n2 * 8, (cuuint64_t)n1 * n2 * 8};
+    cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return bfft_set_error(FFT_E_CUDA, "cuTensorMapEncodeTiled failed: CUresult %d", (int)r);
+    return FFT_OK;
 }
 
 // ------------------------------------------------------------ twiddle tables
@@ -274,7 +320,7 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         stockham_table(ch.n1, ta);
         stockham_table(ch.n2, tb);
     } else if (variant == FFT_VARIANT_FOURSTEP) {
-        if (p->log2n < 2) return bfft_set_error(FFT_E_SIZE, "unsupported transform size for four-step variant: %lld", (long long)n);
+        if (p->log2n < 8) return bfft_set_error(FFT_E_SIZE, "unsupported transform size for four-step variant: %lld", (long long)n);
         const int k1 = p->log2n / 2, k2 = p->log2n - k1;
         p->n1 = 1 << k1;
         p->n2 = 1 << k2;
@@ -392,6 +438,7 @@ extern "C" int fft_plan_get_info(const fft_plan* p, fft_plan_info* info) {
     info->cluster = p->cluster;
     info->scratch_bytes = p->d_scratch ? p->wave * p->n * 8 : 0;
     info->table_bytes = (int64_t)p->tab_bytes;
+    info->resident = p->occ_a;
     if (p->variant == FFT_VARIANT_FOURSTEP)
         info->kernels_per_exec = (int)(2 * ((p->batch + p->wave - 1) / p->wave));
     else
@@ -432,7 +479,11 @@ static int launch(const fft_plan* p, const float2* in, float2* out, int64_t coun
             cfg.stream = st;
             cfg.attrs = at;
             cfg.numAttrs = 1;
-            CUDA_TRY(cudaLaunchKernelEx(&cfg, (ClusterFn)p->ka.fn, in, out, count, p->tw_a, p->tw_b, p->scale));
+            CUtensorMap tm;
+            const int ca = p->n2 / p->cluster;
+            int rc = make_record_tmap(&tm, in, count, p->n1, p->n2, ca, p->n1);
+            if (rc) return rc;
+            CUDA_TRY(cudaLaunchKernelEx(&cfg, (ClusterFn)p->ka.fn, tm, out, count, p->tw_a, p->tw_b, p->scale));
             break;
         }
         case FFT_VARIANT_FOURSTEP: {

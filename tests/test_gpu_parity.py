@@ -50,7 +50,7 @@ def batch_for(n):
 
 SINGLE = [2 ** k for k in range(1, 15)]
 CLUSTER = [2 ** k for k in range(13, 18)]
-FOURSTEP = [2 ** k for k in range(2, 23)]
+FOURSTEP = [2 ** k for k in range(8, 23)]
 
 
 @pytest.mark.parametrize("direction", [-1, 1])
