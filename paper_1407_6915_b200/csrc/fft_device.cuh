@@ -154,25 +154,68 @@ template <> struct Dft<16> {
     }
 };
 
+template <> struct Dft<32> {
+    __device__ __forceinline__ static void run(float2 (&a)[32]) {
+        // radix-2 DIT over two DFT_16: X[k] = E[k] + W_32^k O[k], X[k+16] = E[k] - W_32^k O[k]
+        float2 e[16], o[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            e[i] = a[2 * i];
+            o[i] = a[2 * i + 1];
+        }
+        Dft<16>::run(e);
+        Dft<16>::run(o);
+        constexpr float c[8] = {1.0f,
+                                0.98078528040323043f,  // cos(pi/16)
+                                0.92387953251128674f,  // cos(2pi/16)
+                                0.83146961230254524f,  // cos(3pi/16)
+                                0.70710678118654752f,  // cos(4pi/16)
+                                0.55557023301960218f,  // cos(5pi/16)
+                                0.38268343236508978f,  // cos(6pi/16)
+                                0.19509032201612826f}; // cos(7pi/16)
+#pragma unroll
+        for (int k = 1; k < 16; ++k) {
+            if (k == 8) {
+                o[k] = mul_mi(o[k]);
+            } else {
+                // W_32^k = cos(2 pi k/32) - i sin(2 pi k/32); for k in 9..15 use W_32^{k-8} * (-i)
+                const int kk = k & 7;
+                const float cr = c[kk], si = c[8 - kk == 8 ? 0 : 8 - kk];
+                float2 t = cmul(o[k], make_float2(cr, -si));
+                o[k] = k > 8 ? mul_mi(t) : t;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            a[k] = cadd(e[k], o[k]);
+            a[k + 16] = csub(e[k], o[k]);
+        }
+    }
+};
+
 // ------------------------------------------------------------------ schedule
 __host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
 
-template <int L>
+// Schedule of a length-L transform with up to PP points per thread:
+// P = min(PP, L) points per thread, T = L / P threads per transform, a first
+// pass of radix 2^(log2 L mod log2 P) (if nonzero) and then radix-P passes.
+template <int L, int PP = 16>
 struct Sched {
     static constexpr int K = ilog2(L);
-    static constexpr int P = L < 16 ? L : 16;           // points per thread
+    static constexpr int P = L < PP ? L : PP;           // points per thread
+    static constexpr int KP = ilog2(P);
     static constexpr int T = L / P;                     // threads per record
-    static constexpr int R0 = L <= 16 ? L : ((K & 3) ? (1 << (K & 3)) : 16);
-    static constexpr int NPASS = L <= 16 ? 1 : ((K & 3) ? 1 + K / 4 : K / 4);
+    static constexpr int R0 = L <= PP ? L : ((K % KP) ? (1 << (K % KP)) : P);
+    static constexpr int NPASS = L <= PP ? 1 : ((K % KP) ? 1 + K / KP : K / KP);
     // radix of pass p and sub-length Ns before pass p
-    __host__ __device__ static constexpr int radix(int p) { return p == 0 ? R0 : 16; }
+    __host__ __device__ static constexpr int radix(int p) { return p == 0 ? R0 : P; }
     __host__ __device__ static constexpr int ns(int p) {
-        return p == 0 ? 1 : R0 * (p == 1 ? 1 : (1 << (4 * (p - 1))));
+        return p == 0 ? 1 : R0 * (p == 1 ? 1 : (1 << (KP * (p - 1))));
     }
     // offset (in complex entries) of pass p's twiddle table inside the
-    // per-length table: passes p >= 1 each own 15*Ns entries, [q-1][j mod Ns].
+    // per-length table: passes p >= 1 each own (P-1)*Ns entries, [q-1][j mod Ns].
     __host__ __device__ static constexpr int tw_off(int p) {
-        return p <= 1 ? 0 : tw_off(p - 1) + 15 * ns(p - 1);
+        return p <= 1 ? 0 : tw_off(p - 1) + (P - 1) * ns(p - 1);
     }
     __host__ __device__ static constexpr int tw_entries() { return tw_off(NPASS); }
 };
@@ -186,10 +229,19 @@ struct RowLayout {
 };
 
 // Column layout (engine E2): COLS interleaved transforms, element e of column
-// c at e*COLS + (c ^ (e mod COLS)); a half-warp touches 16 distinct columns
-// of one element row, hence 16 distinct bank pairs.
+// c at e*COLS + c.  Every engine access has a half-warp on 16 consecutive
+// columns of one element row, so it is conflict-free unswizzled — and every
+// address is one per-thread base plus a compile-time offset (no per-element
+// address registers).
 template <int COLS>
 struct ColLayout {
+    __device__ __forceinline__ static int at(int e, int c) { return e * COLS + c; }
+};
+// Swizzled column layout for transposing accesses (a half-warp on 16
+// consecutive elements e of one column): c ^ (e mod COLS) spreads them over
+// 16 distinct bank pairs.
+template <int COLS>
+struct SwzColLayout {
     __device__ __forceinline__ static int at(int e, int c) { return e * COLS + (c ^ (e & (COLS - 1))); }
 };
 
@@ -197,9 +249,9 @@ struct ColLayout {
 // One Stockham pass for a thread holding v[P] = x[t + s*T].  Results are
 // handed to `put(index, value)`; the caller stores them (shared memory, or
 // registers for the last pass).  TW(q, jj) returns W_{Ns*R}^{jj*q}.
-template <int L, int PASS, class Put, class Tw>
-__device__ __forceinline__ void stockham_pass(const float2 (&v)[Sched<L>::P], int t, Put&& put, Tw&& tw) {
-    using S = Sched<L>;
+template <int L, int PP, int PASS, class Put, class Tw>
+__device__ __forceinline__ void stockham_pass(const float2 (&v)[Sched<L, PP>::P], int t, Put&& put, Tw&& tw) {
+    using S = Sched<L, PP>;
     constexpr int P = S::P, T = S::T;
     constexpr int R = S::radix(PASS);
     constexpr int Ns = S::ns(PASS);
@@ -212,8 +264,24 @@ __device__ __forceinline__ void stockham_pass(const float2 (&v)[Sched<L>::P], in
         for (int q = 0; q < R; ++q) a[q] = v[m + q * NB];
         if constexpr (Ns > 1) {
             const int jj = j & (Ns - 1);
+            if constexpr (R <= 16) {
 #pragma unroll
-            for (int q = 1; q < R; ++q) a[q] = cmul(a[q], tw(q, jj));
+                for (int q = 1; q < R; ++q) a[q] = cmul(a[q], tw(q, jj));
+            } else {
+                // radix 32: fetch W^{jj 2^i} (i < 5) and build W^{jj q} as
+                // w[q] = w[q with its lowest set bit cleared] * W^{jj lowbit(q)}
+                // (depth <= 5): 5 live factors instead of 31 loaded twiddles.
+                float2 base[5];
+#pragma unroll
+                for (int i = 0; i < 5; ++i) base[i] = tw(1 << i, jj);
+                float2 w[R];
+#pragma unroll
+                for (int q = 1; q < R; ++q) {
+                    const int lb = (q & 1) ? 0 : (q & 2) ? 1 : (q & 4) ? 2 : (q & 8) ? 3 : 4;
+                    w[q] = (q & (q - 1)) ? cmul(w[q & (q - 1)], base[lb]) : base[lb];
+                    a[q] = cmul(a[q], w[q]);
+                }
+            }
         }
         Dft<R>::run(a);
         const int base = (j / Ns) * Ns * R + (j & (Ns - 1));

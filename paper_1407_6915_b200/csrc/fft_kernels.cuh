@@ -42,12 +42,56 @@ __device__ __forceinline__ float2 twiddle_exact(uint32_t m, uint32_t n) {
 }
 
 // Per-pass Stockham twiddle fetch: table layout [q-1][j mod Ns] per pass.
-template <int L>
+template <int L, int PP = 16>
 struct TableTw {
     const float2* __restrict__ base;  // this length's table
     template <int PASS>
     __device__ __forceinline__ float2 get(int q, int jj) const {
-        return __ldg(base + Sched<L>::tw_off(PASS) + (q - 1) * Sched<L>::ns(PASS) + jj);
+        using S = Sched<L, PP>;
+        return __ldg(base + S::tw_off(PASS) + (q - 1) * S::ns(PASS) + jj);
+    }
+};
+
+// Per-pass Stockham twiddles in constant memory, for the column engines whose
+// butterfly index is warp-uniform (lanes = columns): the constant cache
+// broadcasts and ptxas feeds the values straight into FFMA2 operands, so they
+// cost no registers.  One table per (L, P) pair, filled once per device by the
+// plan layer (bfft_upload_const_twiddles) with the same fp64-computed values.
+__host__ __device__ constexpr int tw_entries_rt(int L, int P) {
+    if (L <= P) return 0;
+    const int K = ilog2(L), KP = ilog2(P);
+    const int R0 = (K % KP) ? (1 << (K % KP)) : P;
+    const int npass = (K % KP) ? 1 + K / KP : K / KP;
+    int tot = 0;
+    for (int p = 1; p < npass; ++p) tot += (P - 1) * R0 * (1 << (KP * (p - 1)));
+    return tot;
+}
+// Lengths with a constant table: P = 16 for L in [32, 2048], P = 32 for L in [64, 512].
+__host__ __device__ constexpr int ctw_max_l(int P) { return P == 16 ? 2048 : 512; }
+constexpr int CTW_MIN_L = 32;
+// offset of the (L, P) table in c_tw; pairs ordered by P in {16, 32}, then L
+__host__ __device__ constexpr int const_tw_base(int L, int P) {
+    int base = 0;
+    for (int p = 16; p <= 32; p *= 2)
+        for (int l = CTW_MIN_L; l <= ctw_max_l(p); l *= 2) {
+            if (l == L && p == P) return base;
+            base += tw_entries_rt(l, p);
+        }
+    return L < 0 ? base : -1;  // L < 0: total size
+}
+constexpr int CTW_TOTAL = const_tw_base(-1, 0);
+static_assert(CTW_TOTAL * 8 <= 60 * 1024, "constant twiddles exceed the constant bank");
+
+__constant__ float2 c_tw[CTW_TOTAL];
+
+template <int L, int PP = 16>
+struct ConstTw {
+    static constexpr int BASE = const_tw_base(L, PP);
+    static_assert(L <= PP || BASE >= 0, "no constant twiddle table for this length");
+    template <int PASS>
+    __device__ __forceinline__ float2 get(int q, int jj) const {
+        using S = Sched<L, PP>;
+        return c_tw[BASE + S::tw_off(PASS) + (q - 1) * S::ns(PASS) + jj];
     }
 };
 
@@ -55,22 +99,22 @@ struct TableTw {
 // v[q] = X[t + q*T] on exit).  Intermediate passes exchange through `sm`
 // addressed by addr(e) (the caller's layout).  Begins each exchange with a
 // CTA barrier, so the buffer may still be read by other threads on entry.
-template <int L, class Addr>
-__device__ __forceinline__ void fft_engine(float2 (&v)[Sched<L>::P], int t, float2* sm,
-                                           Addr&& addr, const TableTw<L>& tw) {
-    using S = Sched<L>;
+template <int L, int PP = 16, class Addr, class Tw>
+__device__ __forceinline__ void fft_engine(float2 (&v)[Sched<L, PP>::P], int t, float2* sm,
+                                           Addr&& addr, const Tw& tw) {
+    using S = Sched<L, PP>;
     constexpr int P = S::P, T = S::T;
     static_for<0, S::NPASS>([&](auto pc) {
         constexpr int PASS = decltype(pc)::value;
         auto twf = [&](int q, int jj) { return tw.template get<PASS>(q, jj); };
         if constexpr (PASS == S::NPASS - 1) {
             float2 o[P];
-            stockham_pass<L, PASS>(v, t, [&](int, int q, int, float2 val) { o[q] = val; }, twf);
+            stockham_pass<L, PP, PASS>(v, t, [&](int, int q, int, float2 val) { o[q] = val; }, twf);
 #pragma unroll
             for (int q = 0; q < P; ++q) v[q] = o[q];
         } else {
             __syncthreads();
-            stockham_pass<L, PASS>(v, t, [&](int idx, int, int, float2 val) { sm[addr(idx)] = val; }, twf);
+            stockham_pass<L, PP, PASS>(v, t, [&](int idx, int, int, float2 val) { sm[addr(idx)] = val; }, twf);
             __syncthreads();
 #pragma unroll
             for (int s = 0; s < P; ++s) v[s] = sm[addr(t + s * T)];
@@ -146,7 +190,7 @@ k_fs_cols(const float2* __restrict__ in, float2* __restrict__ y, int64_t nrec, i
     const int n2 = 1 << log2n2;
     const int tiles = n2 / COLS;
     const uint32_t n = (uint32_t)N1 << log2n2, nmask = n - 1;
-    const TableTw<N1> tab{tw};
+    const ConstTw<N1> tab{};
     auto addr = [&](int e) { return ColLayout<COLS>::at(e, col); };
     for (int64_t g = blockIdx.x; g < nrec * tiles; g += gridDim.x) {
         const int64_t r = g / tiles;
@@ -186,7 +230,7 @@ k_fs_rows(const float2* __restrict__ y, float2* __restrict__ out, int64_t nrec, 
     const int n1 = 1 << log2n1;
     const int tiles = n1 / ROWS;
     const int64_t n = (int64_t)n1 * N2;
-    const TableTw<N2> tab{tw};
+    const ConstTw<N2> tab{};
     auto addr = [&](int e) { return ColLayout<ROWS>::at(e, col); };
     for (int64_t g = blockIdx.x; g < nrec * tiles; g += gridDim.x) {
         const int64_t r = g / tiles;
@@ -197,12 +241,12 @@ k_fs_rows(const float2* __restrict__ y, float2* __restrict__ out, int64_t nrec, 
         for (int u = 0; u < P; ++u) {
             const int i = tid + u * NT;          // linear index in the ROWS x N2 tile
             const int row = i / N2, e = i - (i / N2) * N2;
-            sm[ColLayout<ROWS>::at(e, row)] = ld_stream(src + i);
+            sm[SwzColLayout<ROWS>::at(e, row)] = ld_stream(src + i);
         }
         __syncthreads();
         float2 v[P];
 #pragma unroll
-        for (int s = 0; s < P; ++s) v[s] = sm[addr(t + s * T)];
+        for (int s = 0; s < P; ++s) v[s] = sm[SwzColLayout<ROWS>::at(t + s * T, col)];
         fft_engine<N2>(v, t, sm, addr, tab);
         float2* dst = out + r * n + k0 + col + (int64_t)t * n1;
 #pragma unroll

@@ -62,6 +62,8 @@ using RowFn = void (*)(const float2*, float2*, int64_t, const float2*, float);
 using ColFn = void (*)(const float2*, float2*, int64_t, int, const float2*);
 using RowTFn = void (*)(const float2*, float2*, int64_t, int, const float2*, float);
 using ClusterFn = void (*)(const CUtensorMap, float2*, int64_t, const float2*, const float2*, float);
+using Cluster1Fn = void (*)(const float2*, float2*, int64_t, const float2*, const float2*, float);
+using Cluster2Fn = void (*)(const float2*, float2*, int64_t, float);
 
 template <int L> struct RowGeom {
     static constexpr int T = Sched<L>::T;
@@ -143,7 +145,7 @@ static KernelSet pick_fs_row(int log2l, bool inv) {
 }
 
 struct ClusterChoice {
-    int n1 = 0, n2 = 0, c = 0;
+    int n1 = 0, n2 = 0, c = 0, pp = 16, impl = 0;
     KernelSet k;
 };
 static int cluster_xch() {
@@ -164,8 +166,70 @@ template <int N1, int N2, int C> static ClusterChoice cluster_kernel(bool inv) {
     ch.k.smem = CF::SMEM;
     return ch;
 }
+template <int N1, int N2, int C, int MINB = 0> static ClusterChoice cluster1_kernel(bool inv) {
+    using CF = Cluster1Cfg<N1, N2, C, 32, MINB>;
+    ClusterChoice ch;
+    ch.n1 = N1;
+    ch.n2 = N2;
+    ch.c = C;
+    ch.pp = 32;
+    ch.impl = 1;
+    ch.k.fn = inv ? (const void*)&k_cluster1<N1, N2, C, true, 32, MINB> : (const void*)&k_cluster1<N1, N2, C, false, 32, MINB>;
+    ch.k.threads = CF::NT;
+    ch.k.smem = CF::SMEM;
+    return ch;
+}
+template <int N1, int N2, int C, int PP = 16> static ClusterChoice cluster2_kernel(bool inv) {
+    using CF = Cluster2Cfg<N1, N2, C, PP>;
+    ClusterChoice ch;
+    ch.n1 = N1;
+    ch.n2 = N2;
+    ch.c = C;
+    ch.pp = PP;
+    ch.impl = 2;
+    ch.k.fn = inv ? (const void*)&k_cluster2<N1, N2, C, true, PP> : (const void*)&k_cluster2<N1, N2, C, false, PP>;
+    ch.k.threads = CF::NT;
+    ch.k.smem = CF::SMEM;
+    return ch;
+}
 // Cluster configurations: N = N1*N2 over C CTAs.
+// impl 1 (default): single-buffer k_cluster1; impl 0: TMA-staged k_cluster.
 static ClusterChoice pick_cluster(int log2n, int want_c, bool inv) {
+    // default implementation per size: the fastest measured on B200
+    // (profiles/variants_r01.md): single-buffer k_cluster1 for 2^13..2^15,
+    // TMA-staged k_cluster with st.async exchange and C = 16 for 2^16..2^17.
+    int impl = log2n <= 15 ? 1 : 0;
+    if (const char* e = getenv("BLOCKFFT_CLUSTER_IMPL")) impl = atoi(e);
+    if (impl == 0 && want_c == 0) want_c = 16;
+    if (impl == 2) {
+        switch (log2n) {
+            case 13: return cluster2_kernel<64, 128, 4>(inv);
+            case 14: return cluster2_kernel<128, 128, 4>(inv);
+            case 15: return cluster2_kernel<128, 256, 8>(inv);
+            case 16:
+                if (want_c == 8) return cluster2_kernel<256, 256, 8>(inv);
+                return cluster2_kernel<256, 256, 16>(inv);
+            case 17: return cluster2_kernel<256, 512, 16>(inv);
+            default: return ClusterChoice{};
+        }
+    }
+    int minb = log2n == 16 ? 4 : 0;
+    if (const char* e = getenv("BLOCKFFT_CLUSTER_MINB")) minb = atoi(e);
+    if (impl == 1) {
+        switch (log2n) {
+            case 13: return minb == 4 ? cluster1_kernel<64, 128, 4, 4>(inv) : cluster1_kernel<64, 128, 4, 6>(inv);
+            case 14: return minb == 4 ? cluster1_kernel<128, 128, 4, 4>(inv) : cluster1_kernel<128, 128, 4, 3>(inv);
+            case 15: return minb == 4 ? cluster1_kernel<128, 256, 8, 4>(inv) : cluster1_kernel<128, 256, 8, 3>(inv);
+            case 16:
+                if (want_c == 16) return minb == 4 ? cluster1_kernel<256, 256, 16, 4>(inv) : cluster1_kernel<256, 256, 16, 3>(inv);
+                return minb == 2 ? cluster1_kernel<256, 256, 8, 2>(inv) : cluster1_kernel<256, 256, 8, 1>(inv);
+            case 17:
+                if (want_c == 8) return cluster1_kernel<256, 512, 8, 1>(inv);
+                return minb == 2 ? cluster1_kernel<256, 512, 16, 2>(inv) : cluster1_kernel<256, 512, 16, 1>(inv);
+            case 18: return cluster1_kernel<512, 512, 16, 1>(inv);
+            default: return ClusterChoice{};
+        }
+    }
     switch (log2n) {
         case 13: return cluster_kernel<64, 128, 4>(inv);
         case 14: return cluster_kernel<128, 128, 4>(inv);
@@ -214,19 +278,19 @@ static int make_record_tmap(CUtensorMap* m, const void* base, int64_t count, int
 }
 
 // ------------------------------------------------------------ twiddle tables
-// Stockham per-pass table for length L (same schedule as Sched<L>): for each
-// pass p >= 1 with sub-length Ns, entries [(q-1)*Ns + jj] = W_{16 Ns}^{jj q},
+// Stockham per-pass table for length L (same schedule as Sched<L, P>): for each
+// pass p >= 1 with sub-length Ns, entries [(q-1)*Ns + jj] = W_{P Ns}^{jj q},
 // computed in fp64 and rounded once to fp32.
-static void stockham_table(int L, std::vector<float2>& out) {
+static void stockham_table(int L, std::vector<float2>& out, int P = 16) {
     out.clear();
-    if (L <= 16) return;
-    const int K = ilog2(L);
-    const int R0 = (K & 3) ? (1 << (K & 3)) : 16;
-    const int npass = (K & 3) ? 1 + K / 4 : K / 4;
+    if (L <= P) return;
+    const int K = ilog2(L), KP = ilog2(P);
+    const int R0 = (K % KP) ? (1 << (K % KP)) : P;
+    const int npass = (K % KP) ? 1 + K / KP : K / KP;
     for (int p = 1; p < npass; ++p) {
-        const int Ns = R0 * (1 << (4 * (p - 1)));
-        const int M = 16 * Ns;
-        for (int q = 1; q < 16; ++q)
+        const int Ns = R0 * (1 << (KP * (p - 1)));
+        const int M = P * Ns;
+        for (int q = 1; q < P; ++q)
             for (int jj = 0; jj < Ns; ++jj) {
                 const long long m = (long long)jj * q;  // < M
                 const double ang = -2.0 * M_PI * (double)m / (double)M;
@@ -235,11 +299,34 @@ static void stockham_table(int L, std::vector<float2>& out) {
     }
 }
 
+// Fill c_tw (the constant-memory twiddles of the column engines) once per
+// device, in const_tw_base order.
+#include <mutex>
+static int upload_const_twiddles(int device) {
+    static std::mutex mu;
+    static bool done[256] = {};
+    std::lock_guard<std::mutex> g(mu);
+    if (device < 0 || device >= 256) return bfft_set_error(FFT_E_DEVICE, "device index out of range: %d", device);
+    if (done[device]) return FFT_OK;
+    std::vector<float2> all, one;
+    for (int pp = 16; pp <= 32; pp *= 2)
+        for (int l = CTW_MIN_L; l <= ctw_max_l(pp); l *= 2) {
+            if (const_tw_base(l, pp) != (int)all.size())
+                return bfft_set_error(FFT_E_CUDA, "constant twiddle layout mismatch at L=%d P=%d", l, pp);
+            stockham_table(l, one, pp);
+            all.insert(all.end(), one.begin(), one.end());
+        }
+    if ((int)all.size() != CTW_TOTAL) return bfft_set_error(FFT_E_CUDA, "constant twiddle size mismatch");
+    CUDA_TRY(cudaMemcpyToSymbol(c_tw, all.data(), all.size() * sizeof(float2)));
+    done[device] = true;
+    return FFT_OK;
+}
+
 // ------------------------------------------------------------ the plan
 struct fft_plan {
     int64_t n = 0, batch = 0;
     int dir = 0, variant = 0, device = 0, log2n = 0, sms = 0;
-    int n1 = 0, n2 = 0, cluster = 1;
+    int n1 = 0, n2 = 0, cluster = 1, cluster_impl = 0;
     float scale = 1.f;
     float2* d_tab = nullptr;          // all twiddle tables
     size_t tab_bytes = 0;
@@ -267,7 +354,7 @@ static int default_variant(int log2n) {
         if (v >= 1 && v <= 3) return v;
     }
     if (log2n <= 12) return FFT_VARIANT_SINGLE;
-    if (log2n <= 17) return FFT_VARIANT_CLUSTER;
+    if (log2n <= 18) return FFT_VARIANT_CLUSTER;
     return FFT_VARIANT_FOURSTEP;
 }
 
@@ -294,6 +381,8 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
     CUDA_TRY(cudaGetDevice(&p->device));
     CUDA_TRY(cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, p->device));
     const bool inv = dir == FFT_INVERSE;
+    rc = upload_const_twiddles(p->device);
+    if (rc) return rc;
     if (dir == 0) variant = FFT_VARIANT_IDENTITY;
     if (variant == FFT_VARIANT_AUTO) variant = default_variant(p->log2n);
     p->variant = variant;
@@ -309,7 +398,7 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         p->n2 = 1;
         stockham_table((int)n, ta);
     } else if (variant == FFT_VARIANT_CLUSTER) {
-        int want = 8;
+        int want = 0;
         if (const char* e = getenv("BLOCKFFT_CLUSTER_SIZE")) want = atoi(e);
         ClusterChoice ch = pick_cluster(p->log2n, want, inv);
         if (!ch.k.fn) return bfft_set_error(FFT_E_SIZE, "unsupported transform size for cluster variant: %lld", (long long)n);
@@ -317,8 +406,9 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         p->n1 = ch.n1;
         p->n2 = ch.n2;
         p->cluster = ch.c;
-        stockham_table(ch.n1, ta);
-        stockham_table(ch.n2, tb);
+        p->cluster_impl = ch.impl;
+        stockham_table(ch.n1, ta, ch.pp);
+        stockham_table(ch.n2, tb, ch.pp);
     } else if (variant == FFT_VARIANT_FOURSTEP) {
         if (p->log2n < 8) return bfft_set_error(FFT_E_SIZE, "unsupported transform size for four-step variant: %lld", (long long)n);
         const int k1 = p->log2n / 2, k2 = p->log2n - k1;
@@ -479,11 +569,17 @@ static int launch(const fft_plan* p, const float2* in, float2* out, int64_t coun
             cfg.stream = st;
             cfg.attrs = at;
             cfg.numAttrs = 1;
-            CUtensorMap tm;
-            const int ca = p->n2 / p->cluster;
-            int rc = make_record_tmap(&tm, in, count, p->n1, p->n2, ca, p->n1);
-            if (rc) return rc;
-            CUDA_TRY(cudaLaunchKernelEx(&cfg, (ClusterFn)p->ka.fn, tm, out, count, p->tw_a, p->tw_b, p->scale));
+            if (p->cluster_impl == 2) {
+                CUDA_TRY(cudaLaunchKernelEx(&cfg, (Cluster2Fn)p->ka.fn, in, out, count, p->scale));
+            } else if (p->cluster_impl == 1) {
+                CUDA_TRY(cudaLaunchKernelEx(&cfg, (Cluster1Fn)p->ka.fn, in, out, count, p->tw_a, p->tw_b, p->scale));
+            } else {
+                CUtensorMap tm;
+                const int ca = p->n2 / p->cluster;
+                int rc = make_record_tmap(&tm, in, count, p->n1, p->n2, ca, p->n1);
+                if (rc) return rc;
+                CUDA_TRY(cudaLaunchKernelEx(&cfg, (ClusterFn)p->ka.fn, tm, out, count, p->tw_a, p->tw_b, p->scale));
+            }
             break;
         }
         case FFT_VARIANT_FOURSTEP: {
