@@ -222,10 +222,13 @@ struct Sched {
 
 // --------------------------------------------------------- shared layouts
 // Row layout (engine E1): records contiguous, element e of record b at
-// b*L + e, XOR-swizzled inside 16-element groups (8-byte elements: the bank
-// pair of an element is its index mod 16).
+// lin = b*L + e stored at lin + lin/16 (one pad slot per 16 elements).  The
+// stride-16 writes of a first pass and the unit-stride reads land on 16
+// distinct bank pairs (tools/proto_indexing.py), and every address is a
+// per-thread base plus a compile-time offset.
 struct RowLayout {
-    __device__ __forceinline__ static int at(int lin) { return lin ^ ((lin >> 4) & 15); }
+    __device__ __forceinline__ static int at(int lin) { return lin + (lin >> 4); }
+    __host__ __device__ static constexpr int size(int n) { return n + n / 16; }
 };
 
 // Column layout (engine E2): COLS interleaved transforms, element e of column
@@ -264,16 +267,18 @@ __device__ __forceinline__ void stockham_pass(const float2 (&v)[Sched<L, PP>::P]
         for (int q = 0; q < R; ++q) a[q] = v[m + q * NB];
         if constexpr (Ns > 1) {
             const int jj = j & (Ns - 1);
-            if constexpr (R <= 16) {
+            if constexpr (R <= 8) {
 #pragma unroll
                 for (int q = 1; q < R; ++q) a[q] = cmul(a[q], tw(q, jj));
             } else {
-                // radix 32: fetch W^{jj 2^i} (i < 5) and build W^{jj q} as
+                // radix 16/32: fetch W^{jj 2^i} (i < log2 R) and build W^{jj q} as
                 // w[q] = w[q with its lowest set bit cleared] * W^{jj lowbit(q)}
-                // (depth <= 5): 5 live factors instead of 31 loaded twiddles.
-                float2 base[5];
+                // (depth <= log2 R): log2 R live factors instead of R-1 loaded
+                // twiddles (registers), log2 R loads instead of R-1 (L1/LSU).
+                constexpr int LR = ilog2(R);
+                float2 base[LR];
 #pragma unroll
-                for (int i = 0; i < 5; ++i) base[i] = tw(1 << i, jj);
+                for (int i = 0; i < LR; ++i) base[i] = tw(1 << i, jj);
                 float2 w[R];
 #pragma unroll
                 for (int q = 1; q < R; ++q) {

@@ -69,7 +69,7 @@ template <int L> struct RowGeom {
     static constexpr int T = Sched<L>::T;
     static constexpr int B = T >= 256 ? 1 : 256 / T;  // records per CTA
     static constexpr int THREADS = B * T;
-    static constexpr size_t SMEM = Sched<L>::NPASS > 1 ? sizeof(float2) * B * L : 0;
+    static constexpr size_t SMEM = Sched<L>::NPASS > 1 ? sizeof(float2) * RowLayout::size(B * L) : 0;
 };
 template <int L> struct FsGeom {
     static constexpr int COLS = L >= 2048 ? 8 : 16;   // tile width (columns or rows)
@@ -196,9 +196,9 @@ template <int N1, int N2, int C, int PP = 16> static ClusterChoice cluster2_kern
 // impl 1 (default): single-buffer k_cluster1; impl 0: TMA-staged k_cluster.
 static ClusterChoice pick_cluster(int log2n, int want_c, bool inv) {
     // default implementation per size: the fastest measured on B200
-    // (profiles/variants_r01.md): single-buffer k_cluster1 for 2^13..2^15,
-    // TMA-staged k_cluster with st.async exchange and C = 16 for 2^16..2^17.
-    int impl = log2n <= 15 ? 1 : 0;
+    // (profiles/variants_r01.md): single-buffer k_cluster1 for 2^13..2^15 and
+    // 2^18, TMA-staged k_cluster with st.async exchange and C = 16 for 2^16..2^17.
+    int impl = (log2n <= 15 || log2n >= 18) ? 1 : 0;
     if (const char* e = getenv("BLOCKFFT_CLUSTER_IMPL")) impl = atoi(e);
     if (impl == 0 && want_c == 0) want_c = 16;
     if (impl == 2) {

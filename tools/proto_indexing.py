@@ -76,8 +76,8 @@ def wavefronts(addrs):
         tot += max(len(s) for s in banks.values())
     return tot
 
-def swz_row(e):      # E1 (contiguous rows) swizzle: permute within 16-element groups
-    return e ^ ((e >> 4) & 15)
+def swz_row(e):      # E1 (contiguous rows) layout: one pad slot per 16 elements
+    return e + (e >> 4)
 
 worst = 0
 bad = set()
