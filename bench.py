@@ -264,7 +264,8 @@ def main():
     avg_launch_s = statistics.mean(launch_ms) * 1e-3
     kernels_per_exec = info["kernels_per_exec"]
     achieved = alg_bytes / avg_launch_s / 1e9
-    kname = {"cluster": "k_cluster", "single": "k_rows", "fourstep": "k_fs", "identity": "k_copy"}[info["variant_name"]]
+    kname = {"cluster": "k_cluster", "single": "k_rows", "fourstep": "k_fs", "identity": "k_copy",
+             "pipe": "k_pipe"}[info["variant_name"]]
     traffic, traffic_src = ncu_traffic(kname, n, batch)
 
     # end to end through the public C ABI with pinned host buffers

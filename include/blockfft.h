@@ -62,8 +62,11 @@ enum fft_variant {
                                  exchanging through DSMEM, 2^10 <= N <= 2^17   */
     FFT_VARIANT_FOURSTEP = 3, /* two kernels (column FFT + twiddle, row FFT +
                                  transposed store) through HBM scratch, N >= 256 */
-    FFT_VARIANT_IDENTITY = 4  /* copy kernel: out = in bit-exactly (pipeline
+    FFT_VARIANT_IDENTITY = 4, /* copy kernel: out = in bit-exactly (pipeline
                                  test mode)                      */
+    FFT_VARIANT_PIPE = 5      /* four-step as ONE persistent dependency-driven
+                                 kernel, intermediate in an L2-resident ring,
+                                 2^14 <= N <= 2^22                            */
 };
 
 typedef struct fft_plan fft_plan; /* opaque */

@@ -17,7 +17,7 @@ import os
 
 from . import _abi
 from ._abi import (FFT_FORWARD, FFT_IDENTITY, FFT_INVERSE, VARIANT_AUTO, VARIANT_CLUSTER,  # noqa: F401
-                   VARIANT_FOURSTEP, VARIANT_IDENTITY, VARIANT_NAMES, VARIANT_SINGLE)
+                   VARIANT_FOURSTEP, VARIANT_IDENTITY, VARIANT_NAMES, VARIANT_PIPE, VARIANT_SINGLE)
 
 _lib = _abi.lib
 

@@ -21,8 +21,8 @@ FFT_OK, FFT_E_SIZE, FFT_E_BATCH, FFT_E_DIR, FFT_E_ARG, FFT_E_DEVICE, FFT_E_CUDA,
 STATUS_NAMES = ["FFT_OK", "FFT_E_SIZE", "FFT_E_BATCH", "FFT_E_DIR", "FFT_E_ARG", "FFT_E_DEVICE",
                 "FFT_E_CUDA", "FFT_E_NOMEM", "FFT_E_IO", "FFT_E_EMPTY"]
 
-VARIANT_AUTO, VARIANT_SINGLE, VARIANT_CLUSTER, VARIANT_FOURSTEP, VARIANT_IDENTITY = range(5)
-VARIANT_NAMES = {0: "auto", 1: "single", 2: "cluster", 3: "fourstep", 4: "identity"}
+VARIANT_AUTO, VARIANT_SINGLE, VARIANT_CLUSTER, VARIANT_FOURSTEP, VARIANT_IDENTITY, VARIANT_PIPE = range(6)
+VARIANT_NAMES = {0: "auto", 1: "single", 2: "cluster", 3: "fourstep", 4: "identity", 5: "pipe"}
 
 # Every symbol include/blockfft.h declares (checked by tests/test_abi.py).
 EXPORTED = ["fft_plan_create", "fft_plan_create_ex", "fft_exec", "fft_exec_range",

@@ -144,8 +144,14 @@ __device__ __forceinline__ void twiddle_row16(uint32_t m0, uint32_t dm, uint32_t
 // ======================================================================
 // E1: single-pass, B records per CTA, one record = T threads x P points.
 // ======================================================================
+template <int L, int B>
+struct RowsMinBlocks {  // CTAs per SM the register budget is sized for
+    static constexpr int THREADS = B * Sched<L>::T;
+    static constexpr int V = THREADS <= 256 ? 3 : 1;
+};
+
 template <int L, int B, bool INV>
-__global__ void __launch_bounds__(B * Sched<L>::T)
+__global__ void __launch_bounds__(B * Sched<L>::T, RowsMinBlocks<L, B>::V)
 k_rows(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
        const float2* __restrict__ tw, float scale) {
     using S = Sched<L>;

@@ -1,0 +1,209 @@
+// fft_pipe.cuh — the four-step as ONE persistent,
+// dependency-driven kernel whose intermediate stays in L2.
+//
+// N = N1 * N2, n = N2 n1 + n2, k = k1 + N1 k2:
+//   A-task (record r, column tile c0..c0+COLS):
+//       Y[k1][n2] = W_N^{n2 k1} * FFT_N1 over n1 of x[N2 n1 + n2]   -> ring slot r mod S
+//   B-task (record r, row tile k0..k0+ROWS):
+//       X[k1 + N1 k2] = FFT_N2 over n2 of Y[k1][n2]                  -> output
+// Tasks are handed out in rounds by one global atomic counter: round s holds
+// the A-tasks of record s and then the B-tasks of record s - LAG.  A B-task
+// waits (acquire) until every A-task of its record has published; an A-task
+// waits until the B-tasks of the record that last used its ring slot have
+// read it.  Every dependency points to an earlier-issued task held by a
+// running CTA, so the schedule cannot deadlock, and CTAs never idle at a
+// grid-wide barrier.  The ring is S records (S N 8 bytes, sized to stay in
+// the 126 MB L2): HBM sees x once and X once (16 N bytes per record, the
+// algorithmic minimum) while the transpose traffic stays on chip.
+#pragma once
+
+#include "fft_kernels.cuh"
+
+namespace bfft {
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_gpu(int* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_geq(const int* p, int target) {
+    if (ld_acquire_gpu(p) >= target) return;
+    int ns = 32;
+    while (ld_acquire_gpu(p) < target) {
+        __nanosleep(ns);
+        ns = ns < 1024 ? 2 * ns : ns;
+    }
+}
+__device__ __forceinline__ float2 ld_l2(const float2* p) { return __ldcg(p); }
+
+// W_N^m from the plan's two-level table (fp64-computed, fp32-rounded):
+// W^m = hi[m >> LB] * lo[m & (2^LB - 1)], one extra rounding.
+struct TwoLevel {
+    const float2* __restrict__ hi;
+    const float2* __restrict__ lo;
+    int lb;
+    uint32_t nmask;
+    __device__ __forceinline__ float2 operator()(uint32_t m) const {
+        m &= nmask;
+        return cmul(__ldg(hi + (m >> lb)), __ldg(lo + (m & ((1u << lb) - 1))));
+    }
+};
+
+template <int N1, int N2, int COLS, int ROWS>
+struct PipeCfg {
+    static constexpr int N = N1 * N2;
+    static constexpr int NT = COLS * Sched<N1>::T;
+    static_assert(ROWS * Sched<N2>::T == NT, "A and B tasks use the same block");
+    static_assert(Sched<N1>::P == 16 && Sched<N2>::P == 16, "N1, N2 >= 16");
+    static constexpr int TA = N2 / COLS;  // A-tasks per record
+    static constexpr int TB = N1 / ROWS;  // B-tasks per record
+    static constexpr int SM_ENTRIES = (COLS * N1 > ROWS * N2 ? COLS * N1 : ROWS * N2);
+    static constexpr size_t SMEM = sizeof(float2) * SM_ENTRIES + 16;
+    static constexpr int MINB_RAW = 65536 / (NT * 64);  // registers per thread >= 64
+    static constexpr int MINB = MINB_RAW < 1 ? 1 : (MINB_RAW > 8 ? 8 : MINB_RAW);
+};
+
+// Optional phase timing (experiments only: tools/exp/exp_pipe.cu defines
+// BFFT_PIPE_PROF; the product library never does).
+#ifdef BFFT_PIPE_PROF
+__device__ unsigned long long g_pipe_prof[16];
+#define PIPE_T(i) unsigned long long _t##i = 0; if (tid == 0) _t##i = clock64();
+#define PIPE_ACC(slot, a, b) if (tid == 0) atomicAdd(&g_pipe_prof[slot], _t##b - _t##a);
+#else
+#define PIPE_T(i)
+#define PIPE_ACC(slot, a, b)
+#endif
+
+// ctr layout (int32): [0] task counter, [1 .. S] A-tasks published per slot,
+// [S+1 .. 2S] B-tasks finished reading per slot (cumulative across reuses).
+template <int N1, int N2, int COLS, int ROWS, bool INV>
+__global__ void __launch_bounds__(PipeCfg<N1, N2, COLS, ROWS>::NT, PipeCfg<N1, N2, COLS, ROWS>::MINB)
+k_pipe(const float2* __restrict__ in, float2* __restrict__ out, float2* __restrict__ ring, int64_t nrec,
+       int* __restrict__ ctr, int S, int LAG, float scale, const float2* __restrict__ w_hi,
+       const float2* __restrict__ w_lo, int w_lb) {
+    using CF = PipeCfg<N1, N2, COLS, ROWS>;
+    constexpr int N = CF::N, TA = CF::TA, TB = CF::TB;
+    constexpr int TA1 = Sched<N1>::T, TB2 = Sched<N2>::T;
+    constexpr int NT = CF::NT;
+    extern __shared__ __align__(128) float2 sm[];
+    __shared__ int s_task;
+    const int tid = threadIdx.x;
+    int* doneA = ctr + 1;
+    int* doneB = ctr + 1 + S;
+    const int64_t per_round = TA + TB;
+    const int64_t total = (nrec + LAG) * per_round;
+    const ConstTw<N1> tabA{};
+    const ConstTw<N2> tabB{};
+    const TwoLevel W{w_hi, w_lo, w_lb, (uint32_t)(N - 1)};
+
+    // The next task index is claimed while the current task runs (its atomic
+    // round trip to L2 is off the critical path).
+    int next = 0;
+    if (tid == 0) next = atomicAdd(ctr, 1);
+    for (;;) {
+        __syncthreads();  // s_task and shared memory of the previous task are free
+        if (tid == 0) {
+            s_task = next;
+            if (next < total) next = atomicAdd(ctr, 1);
+        }
+        __syncthreads();
+        const int64_t task = s_task;
+        if (task >= total) break;
+        PIPE_T(0)
+        const int64_t round = task / per_round;
+        const int o = (int)(task - round * per_round);
+        if (o < TA) {
+            // ================================================ A-task
+            const int64_t r = round;
+            if (r >= nrec) continue;
+            const int slot = (int)(r % S);
+            const int gen = (int)(r / S);
+            const int col = tid % COLS, t = tid / COLS;
+            const int n2 = o * COLS + col;
+            const float2* src = in + r * N + n2 + (int64_t)t * N2;
+            float2 v[16];
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                const float2 x = ld_stream(src + (int64_t)s * TA1 * N2);
+                v[s] = INV ? conjf2(x) : x;
+            }
+            // W_N^{n2 k1} factors, fetched before the engine so their latency hides behind it
+            float2 f[4], w0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) f[i] = W((uint32_t)n2 * (uint32_t)(TA1 << i));
+            w0 = W((uint32_t)n2 * (uint32_t)t);
+            fft_engine<N1>(v, t, sm, [&](int e) { return ColLayout<COLS>::at(e, col); }, tabA);
+            PIPE_T(1)
+            // k1 = t + q TA1: w[q] = w[q without its lowest bit] * f[lowbit]
+            {
+                float2 w[16];
+                w[0] = w0;
+                v[0] = cmul(v[0], w[0]);
+#pragma unroll
+                for (int q = 1; q < 16; ++q) {
+                    const int lb = (q & 1) ? 0 : (q & 2) ? 1 : (q & 4) ? 2 : 3;
+                    w[q] = cmul(w[q & (q - 1)], f[lb]);
+                    v[q] = cmul(v[q], w[q]);
+                }
+            }
+            PIPE_T(2)
+            // the slot's previous record must have been read by all its B-tasks
+            if (gen > 0) {
+                if (tid == 0) wait_geq(doneB + slot, gen * TB);
+                __syncthreads();
+            }
+            PIPE_T(3)
+            float2* dst = ring + (int64_t)slot * N + n2 + (int64_t)t * N2;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) dst[(int64_t)q * TA1 * N2] = v[q];
+            __syncthreads();
+            if (tid == 0) red_release_gpu(doneA + slot, 1);
+            PIPE_T(4)
+            PIPE_ACC(0, 0, 1) PIPE_ACC(1, 1, 2) PIPE_ACC(2, 2, 3) PIPE_ACC(3, 3, 4)
+            if (tid == 0) { PIPE_ACC(4, 0, 4) }
+#ifdef BFFT_PIPE_PROF
+            if (tid == 0) atomicAdd(&g_pipe_prof[10], 1ull);
+#endif
+        } else {
+            // ================================================ B-task
+            const int64_t r = round - LAG;
+            if (r < 0 || r >= nrec) continue;
+            const int b = o - TA;
+            const int slot = (int)(r % S);
+            const int gen = (int)(r / S);
+            const int k0 = b * ROWS;
+            if (tid == 0) wait_geq(doneA + slot, (gen + 1) * TA);
+            __syncthreads();
+            PIPE_T(5)
+            const float2* src = ring + (int64_t)slot * N + (int64_t)k0 * N2;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int i = tid + u * NT;  // linear index in the ROWS x N2 tile
+                const int row = i / N2, e = i - (i / N2) * N2;
+                sm[SwzColLayout<ROWS>::at(e, row)] = ld_l2(src + i);
+            }
+            __syncthreads();
+            if (tid == 0) red_release_gpu(doneB + slot, 1);  // slot rows read: A-tasks may reuse
+            PIPE_T(6)
+            const int col = tid % ROWS, t = tid / ROWS;
+            float2 v[16];
+#pragma unroll
+            for (int s = 0; s < 16; ++s) v[s] = sm[SwzColLayout<ROWS>::at(t + s * TB2, col)];
+            fft_engine<N2>(v, t, sm, [&](int e) { return ColLayout<ROWS>::at(e, col); }, tabB);
+            float2* dst = out + r * N + k0 + col + (int64_t)t * N1;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                st_stream(dst + (int64_t)q * TB2 * N1, INV ? scale_conj(v[q], scale) : v[q]);
+            PIPE_T(7)
+            PIPE_ACC(5, 0, 5) PIPE_ACC(6, 5, 6) PIPE_ACC(7, 6, 7) PIPE_ACC(8, 0, 7)
+#ifdef BFFT_PIPE_PROF
+            if (tid == 0) atomicAdd(&g_pipe_prof[11], 1ull);
+#endif
+        }
+    }
+}
+
+}  // namespace bfft

@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 
 #include "fft_cluster.cuh"
+#include "fft_pipe.cuh"
 #include "fft_kernels.cuh"
 
 using namespace bfft;
@@ -64,6 +65,8 @@ using RowTFn = void (*)(const float2*, float2*, int64_t, int, const float2*, flo
 using ClusterFn = void (*)(const CUtensorMap, float2*, int64_t, const float2*, const float2*, float);
 using Cluster1Fn = void (*)(const float2*, float2*, int64_t, const float2*, const float2*, float);
 using Cluster2Fn = void (*)(const float2*, float2*, int64_t, float);
+using PipeFn = void (*)(const float2*, float2*, float2*, int64_t, int*, int, int, float, const float2*,
+                        const float2*, int);
 
 template <int L> struct RowGeom {
     static constexpr int T = Sched<L>::T;
@@ -242,6 +245,40 @@ static ClusterChoice pick_cluster(int log2n, int want_c, bool inv) {
     }
 }
 
+struct PipeChoice {
+    int n1 = 0, n2 = 0, cols = 0, rows = 0;
+    KernelSet k;
+};
+template <int N1, int N2, int COLS, int ROWS> static PipeChoice pipe_kernel(bool inv) {
+    using CF = PipeCfg<N1, N2, COLS, ROWS>;
+    PipeChoice ch;
+    ch.n1 = N1;
+    ch.n2 = N2;
+    ch.cols = COLS;
+    ch.rows = ROWS;
+    ch.k.fn = inv ? (const void*)&k_pipe<N1, N2, COLS, ROWS, true> : (const void*)&k_pipe<N1, N2, COLS, ROWS, false>;
+    ch.k.threads = CF::NT;
+    ch.k.smem = CF::SMEM;
+    return ch;
+}
+// Pipelined four-step splits (N1 >= N2; A-tile COLS columns, B-tile ROWS rows).
+static PipeChoice pick_pipe(int log2n, bool inv) {
+    switch (log2n) {
+        case 14: return pipe_kernel<128, 128, 16, 16>(inv);
+        case 15: return pipe_kernel<256, 128, 32, 64>(inv);
+        case 16:
+            if (getenv("BLOCKFFT_PIPE_WIDE")) return pipe_kernel<256, 256, 32, 32>(inv);
+            return pipe_kernel<256, 256, 16, 16>(inv);
+        case 17: return pipe_kernel<512, 256, 16, 32>(inv);
+        case 18: return pipe_kernel<512, 512, 16, 16>(inv);
+        case 19: return pipe_kernel<1024, 512, 8, 16>(inv);
+        case 20: return pipe_kernel<1024, 1024, 8, 8>(inv);
+        case 21: return pipe_kernel<2048, 1024, 8, 16>(inv);
+        case 22: return pipe_kernel<2048, 2048, 8, 8>(inv);
+        default: return PipeChoice{};
+    }
+}
+
 // ------------------------------------------------------------ TMA tensor maps
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -327,6 +364,9 @@ struct fft_plan {
     int64_t n = 0, batch = 0;
     int dir = 0, variant = 0, device = 0, log2n = 0, sms = 0;
     int n1 = 0, n2 = 0, cluster = 1, cluster_impl = 0;
+    int pipe_S = 0, pipe_LAG = 0;     // pipelined four-step ring depth and lag
+    int w_lb = 0;                     // two-level twiddle split (tw_a = hi, tw_b = lo)
+    int* d_ctr = nullptr;             // pipelined four-step task/dependency counters
     float scale = 1.f;
     float2* d_tab = nullptr;          // all twiddle tables
     size_t tab_bytes = 0;
@@ -351,11 +391,12 @@ static int validate(int64_t n, int64_t batch, int dir) {
 static int default_variant(int log2n) {
     if (const char* e = getenv("BLOCKFFT_VARIANT")) {
         int v = atoi(e);
-        if (v >= 1 && v <= 3) return v;
+        if ((v >= 1 && v <= 3) || v == FFT_VARIANT_PIPE) return v;
     }
+    // fastest measured per size (profiles/r01_variants_*.txt)
     if (log2n <= 12) return FFT_VARIANT_SINGLE;
-    if (log2n <= 18) return FFT_VARIANT_CLUSTER;
-    return FFT_VARIANT_FOURSTEP;
+    if (log2n == 13) return FFT_VARIANT_CLUSTER;
+    return FFT_VARIANT_PIPE;
 }
 
 static int set_smem(const KernelSet& k) {
@@ -371,7 +412,7 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         return bfft_set_error(FFT_E_DIR, "direction 0 (identity) needs the identity variant: %d", variant);
     if (dir != 0 && variant == FFT_VARIANT_IDENTITY)
         return bfft_set_error(FFT_E_DIR, "identity variant takes direction 0: %d", dir);
-    if (variant < 0 || variant > FFT_VARIANT_IDENTITY)
+    if (variant < 0 || variant > FFT_VARIANT_PIPE)
         return bfft_set_error(FFT_E_ARG, "unknown variant: %d", variant);
     p->n = n;
     p->batch = batch;
@@ -409,6 +450,25 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         p->cluster_impl = ch.impl;
         stockham_table(ch.n1, ta, ch.pp);
         stockham_table(ch.n2, tb, ch.pp);
+    } else if (variant == FFT_VARIANT_PIPE) {
+        PipeChoice ch = pick_pipe(p->log2n, inv);
+        if (!ch.k.fn) return bfft_set_error(FFT_E_SIZE, "unsupported transform size for pipelined variant: %lld", (long long)n);
+        p->ka = ch.k;
+        p->n1 = ch.n1;
+        p->n2 = ch.n2;
+        p->ka.cols = ch.cols;
+        p->kb.cols = ch.rows;
+        // two-level W_N table: hi[a] = W_N^{a 2^lb}, lo[b] = W_N^b (fp64 -> fp32)
+        p->w_lb = (p->log2n + 1) / 2;
+        const int nhi = 1 << (p->log2n - p->w_lb), nlo = 1 << p->w_lb;
+        for (int a = 0; a < nhi; ++a) {
+            const double ang = -2.0 * M_PI * (double)((int64_t)a << p->w_lb) / (double)n;
+            ta.push_back(make_float2((float)cos(ang), (float)sin(ang)));
+        }
+        for (int b = 0; b < nlo; ++b) {
+            const double ang = -2.0 * M_PI * (double)b / (double)n;
+            tb.push_back(make_float2((float)cos(ang), (float)sin(ang)));
+        }
     } else if (variant == FFT_VARIANT_FOURSTEP) {
         if (p->log2n < 8) return bfft_set_error(FFT_E_SIZE, "unsupported transform size for four-step variant: %lld", (long long)n);
         const int k1 = p->log2n / 2, k2 = p->log2n - k1;
@@ -466,6 +526,29 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         CUDA_TRY(cudaOccupancyMaxActiveClusters(&ncl, p->ka.fn, &cfg));
         if (ncl < 1) return bfft_set_error(FFT_E_CUDA, "cluster of %d CTAs x %zu B shared memory cannot be scheduled", p->cluster, p->ka.smem);
         p->occ_a = ncl;  // co-resident clusters
+    } else if (variant == FFT_VARIANT_PIPE) {
+        rc = set_smem(p->ka);
+        if (rc) return rc;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ_a, p->ka.fn, p->ka.threads, p->ka.smem));
+        p->occ_a = std::max(p->occ_a, 1);
+        const int resident = p->occ_a * p->sms;
+        const int per_round = p->n2 / p->ka.cols + p->n1 / p->kb.cols;
+        // B-tasks of record r are issued LAG rounds after its A-tasks and an
+        // A-task reuses the slot of record r - S, whose B-tasks were issued
+        // S - LAG rounds earlier: both gaps span ~2 x the resident CTAs, so
+        // dependencies are normally complete when a task starts.  The ring is
+        // capped at 96 MiB to stay resident in the 126 MB L2.
+        p->pipe_LAG = (2 * resident + per_round - 1) / per_round + 1;
+        const int64_t rec_bytes = n * (int64_t)sizeof(float2);
+        const int s_cap = (int)std::max<int64_t>(p->pipe_LAG + 2, (96ll << 20) / rec_bytes);
+        p->pipe_S = std::min(2 * p->pipe_LAG + 1, s_cap);
+        if (const char* e = getenv("BLOCKFFT_PIPE_S")) p->pipe_S = std::max(p->pipe_LAG + 1, atoi(e));
+        const size_t rb = (size_t)p->pipe_S * (size_t)n * sizeof(float2);
+        cudaError_t e = cudaMalloc(&p->d_scratch, rb);
+        if (e != cudaSuccess) return bfft_set_error(FFT_E_NOMEM, "cudaMalloc(%zu) for the pipelined ring failed: %s", rb, cudaGetErrorString(e));
+        e = cudaMalloc(&p->d_ctr, sizeof(int) * (1 + 2 * p->pipe_S));
+        if (e != cudaSuccess) return bfft_set_error(FFT_E_NOMEM, "cudaMalloc for pipelined counters failed: %s", cudaGetErrorString(e));
+        p->wave = p->pipe_S;
     } else if (variant == FFT_VARIANT_FOURSTEP) {
         rc = set_smem(p->ka);
         if (rc) return rc;
@@ -489,6 +572,7 @@ static void plan_free(fft_plan* p) {
     if (!p) return;
     if (p->d_tab) cudaFree(p->d_tab);
     if (p->d_scratch) cudaFree(p->d_scratch);
+    if (p->d_ctr) cudaFree(p->d_ctr);
     delete p;
 }
 
@@ -580,6 +664,14 @@ static int launch(const fft_plan* p, const float2* in, float2* out, int64_t coun
                 if (rc) return rc;
                 CUDA_TRY(cudaLaunchKernelEx(&cfg, (ClusterFn)p->ka.fn, tm, out, count, p->tw_a, p->tw_b, p->scale));
             }
+            break;
+        }
+        case FFT_VARIANT_PIPE: {
+            CUDA_TRY(cudaMemsetAsync(p->d_ctr, 0, sizeof(int) * (1 + 2 * p->pipe_S), st));
+            const int grid = p->occ_a * p->sms;
+            ((PipeFn)p->ka.fn)<<<grid, p->ka.threads, p->ka.smem, st>>>(in, out, p->d_scratch, count, p->d_ctr,
+                                                                       p->pipe_S, p->pipe_LAG, p->scale, p->tw_a,
+                                                                       p->tw_b, p->w_lb);
             break;
         }
         case FFT_VARIANT_FOURSTEP: {

@@ -85,6 +85,27 @@ def test_fourstep(n, direction):
     check(x, direction, bf.VARIANT_FOURSTEP)
 
 
+PIPE = [2 ** k for k in range(14, 23)]
+
+
+@pytest.mark.parametrize("direction", [-1, 1])
+@pytest.mark.parametrize("n", PIPE)
+def test_pipe(n, direction):
+    # more records than the ring holds, so slots are reused (WAR dependencies exercised)
+    b = 3 if n >= (1 << 21) else max(9, min((1 << 21) // n, 129)) | 1
+    x = synth.random_records(synth.DEFAULT_SEED + 5 * n, n, 0, b)
+    check(x, direction, bf.VARIANT_PIPE)
+
+
+def test_pipe_ring_reuse_many_records():
+    n = 1 << 14
+    with bf.Plan(n, 1, bf.FFT_FORWARD, bf.VARIANT_PIPE) as p:
+        s = p.info()["scratch_bytes"] // (8 * n)
+    b = 4 * s + 3
+    x = synth.random_records(31, n, 0, b)
+    check(x, bf.FFT_FORWARD, bf.VARIANT_PIPE)
+
+
 @pytest.mark.parametrize("n", [2, 16, 1024, 4096, 1 << 14, 1 << 16, 1 << 17, 1 << 20])
 def test_auto_roundtrip(n):
     # inverse(forward(x)) ~= x
@@ -118,7 +139,8 @@ def test_closed_forms_on_gpu(variant, n):
     assert np.all(y[4] == 0)                                           # zeros stay exactly zero
 
 
-@pytest.mark.parametrize("variant,n", [(1, 256), (1, 4096), (2, 1 << 16), (2, 1 << 17), (3, 1 << 20)])
+@pytest.mark.parametrize("variant,n", [(1, 256), (1, 4096), (2, 1 << 16), (2, 1 << 17), (3, 1 << 20), (5, 1 << 16),
+                                       (5, 1 << 20)])
 def test_batch_position_bit_identity(variant, n):
     # a record's result does not depend on the batch around it
     b = 7
@@ -140,7 +162,7 @@ def test_full_config2_sampled():
     sg.fill_random(x, seed)
     y = torch.empty_like(x)
     with bf.Plan(n, b) as p:
-        assert p.info()["variant_name"] == "cluster"
+        assert p.info()["variant_name"] in ("cluster", "pipe")
         p.exec(x, y)
     torch.cuda.synchronize()
     idx = synth.sample_indices(b, 24)
