@@ -99,9 +99,20 @@ struct ConstTw {
 // v[q] = X[t + q*T] on exit).  Intermediate passes exchange through `sm`
 // addressed by addr(e) (the caller's layout).  Begins each exchange with a
 // CTA barrier, so the buffer may still be read by other threads on entry.
-template <int L, int PP = 16, class Addr, class Tw>
+struct CtaBarrier {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+// Named barrier over the first `count` threads of the CTA (warp-specialised kernels).
+struct NamedBarrier {
+    int id, count;
+    __device__ __forceinline__ void operator()() const {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+    }
+};
+
+template <int L, int PP = 16, class Addr, class Tw, class Bar = CtaBarrier>
 __device__ __forceinline__ void fft_engine(float2 (&v)[Sched<L, PP>::P], int t, float2* sm,
-                                           Addr&& addr, const Tw& tw) {
+                                           Addr&& addr, const Tw& tw, Bar bar = Bar{}) {
     using S = Sched<L, PP>;
     constexpr int P = S::P, T = S::T;
     static_for<0, S::NPASS>([&](auto pc) {
@@ -113,9 +124,9 @@ __device__ __forceinline__ void fft_engine(float2 (&v)[Sched<L, PP>::P], int t, 
 #pragma unroll
             for (int q = 0; q < P; ++q) v[q] = o[q];
         } else {
-            __syncthreads();
+            bar();
             stockham_pass<L, PP, PASS>(v, t, [&](int idx, int, int, float2 val) { sm[addr(idx)] = val; }, twf);
-            __syncthreads();
+            bar();
 #pragma unroll
             for (int s = 0; s < P; ++s) v[s] = sm[addr(t + s * T)];
         }

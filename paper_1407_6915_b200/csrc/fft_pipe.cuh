@@ -17,6 +17,7 @@
 // algorithmic minimum) while the transpose traffic stays on chip.
 #pragma once
 
+#include "fft_cluster.cuh"
 #include "fft_kernels.cuh"
 
 namespace bfft {
@@ -69,7 +70,14 @@ struct PipeCfg {
 // Optional phase timing (experiments only: tools/exp/exp_pipe.cu defines
 // BFFT_PIPE_PROF; the product library never does).
 #ifdef BFFT_PIPE_PROF
-__device__ unsigned long long g_pipe_prof[16];
+__device__ unsigned long long g_pipe_prof[32];
+#define P2_T(v) unsigned long long v = clock64();
+#define P2_ACC(slot, a, b) atomicAdd(&g_pipe_prof[slot], (b) - (a));
+#else
+#define P2_T(v)
+#define P2_ACC(slot, a, b)
+#endif
+#ifdef BFFT_PIPE_PROF
 #define PIPE_T(i) unsigned long long _t##i = 0; if (tid == 0) _t##i = clock64();
 #define PIPE_ACC(slot, a, b) if (tid == 0) atomicAdd(&g_pipe_prof[slot], _t##b - _t##a);
 #else
@@ -202,6 +210,251 @@ k_pipe(const float2* __restrict__ in, float2* __restrict__ out, float2* __restri
 #ifdef BFFT_PIPE_PROF
             if (tid == 0) atomicAdd(&g_pipe_prof[11], 1ull);
 #endif
+        }
+    }
+}
+
+}  // namespace bfft
+
+namespace bfft {
+
+// ======================================================================
+// k_pipe2: the same task graph as k_pipe, warp-specialised so that no
+// memory latency sits on the compute warps' critical path.
+//   producer warp : claims tasks, waits for their dependencies, and loads
+//                   each task's tile into an NSTAGE-deep shared-memory ring
+//                   with TMA (A-tile: one tensor box per 256 rows of the
+//                   record's column tile; B-tile: one bulk copy per ring row
+//                   into a padded row) completing on full[stage];
+//   compute warps : FFT the staged tile (exchanges inside the same stage
+//                   buffer, consumer-only named barrier), apply twiddles,
+//                   store, arrive done[stage];
+//   release warp  : once a task's stores are issued, publishes it with
+//                   fence.acq_rel.gpu + red (the ~us fence latency stays off
+//                   the compute warps), then frees the stage.
+// ======================================================================
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void red_relaxed_gpu(int* p, int v) {
+    asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int N1, int N2, int COLS, int ROWS, int NSTAGE>
+struct Pipe2Cfg {
+    static constexpr int N = N1 * N2;
+    static constexpr int NTC = COLS * Sched<N1>::T;            // compute threads
+    static_assert(ROWS * Sched<N2>::T == NTC, "A and B tasks use the same compute warps");
+    static_assert(NTC % 32 == 0, "whole compute warps");
+    static constexpr int NT = NTC + 64;                          // + producer warp + release warp
+    static constexpr int TA = N2 / COLS, TB = N1 / ROWS;
+    static constexpr int RSTRIDE = N2 + 2;                       // padded B-tile row (16-B multiple)
+    static constexpr int TILE_A = COLS * N1, TILE_B = ROWS * RSTRIDE;
+    static constexpr int TILE = TILE_A > TILE_B ? TILE_A : TILE_B;
+    static constexpr int BOXR = N1 < 256 ? N1 : 256;             // TMA box rows
+    static constexpr size_t SMEM = sizeof(float2) * (size_t)TILE * NSTAGE + 64 * NSTAGE + 128;
+    static constexpr int MINB_RAW = 65536 / (NT * 64);
+    static constexpr int MINB = MINB_RAW < 1 ? 1 : (MINB_RAW > 8 ? 8 : MINB_RAW);
+};
+
+struct PipeTask {
+    long long rec;  // record index
+    int kind;       // 0 = A, 1 = B, 2 = end
+    int tile;       // column tile (A) or row tile (B)
+};
+
+template <int N1, int N2, int COLS, int ROWS, bool INV, int NSTAGE>
+__global__ void __launch_bounds__(Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE>::NT, Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE>::MINB)
+k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, float2* __restrict__ ring,
+        int64_t nrec, int* __restrict__ ctr, int S, int LAG, float scale, const float2* __restrict__ w_hi,
+        const float2* __restrict__ w_lo, int w_lb) {
+    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE>;
+    constexpr int N = CF::N, TA = CF::TA, TB = CF::TB, NTC = CF::NTC, TILE = CF::TILE, RSTRIDE = CF::RSTRIDE;
+    constexpr int TA1 = Sched<N1>::T, TB2 = Sched<N2>::T;
+    extern __shared__ __align__(128) float2 sm[];
+    PipeTask* info = reinterpret_cast<PipeTask*>(sm + (size_t)TILE * NSTAGE);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(info + NSTAGE);   // full | empty | done
+    const uint32_t full0 = smem_addr(bars), empty0 = smem_addr(bars + NSTAGE), done0 = smem_addr(bars + 2 * NSTAGE);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int WP = NTC / 32, WR = NTC / 32 + 1;  // producer, release warps
+    int* doneA = ctr + 1;
+    int* doneB = ctr + 1 + S;
+    const int64_t per_round = TA + TB;
+    const int64_t total = (nrec + LAG) * per_round;
+
+    if (tid == 0) {
+        for (int i = 0; i < NSTAGE; ++i) {
+            mbar_init(full0 + 8 * i, 1);
+            mbar_init(empty0 + 8 * i, 1);       // the release warp frees a stage
+            mbar_init(done0 + 8 * i, NTC / 32); // one arrival per compute warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == WP) {
+        // ============================================== producer
+        if (lane == 0) {
+            uint32_t k = 0;
+            // the claim of the next task is in flight while this one is staged
+            long long next = atomicAdd(ctr, 1);
+            for (;;) {
+                const long long task = next;
+                if (task < total) next = atomicAdd(ctr, 1);
+                PipeTask d;
+                bool valid = true;
+                if (task >= total) {
+                    d.kind = 2;
+                    d.rec = 0;
+                    d.tile = 0;
+                } else {
+                    const long long round = task / per_round;
+                    const int o = (int)(task - round * per_round);
+                    if (o < TA) {
+                        d.kind = 0;
+                        d.rec = round;
+                        d.tile = o;
+                        valid = round < nrec;
+                    } else {
+                        d.kind = 1;
+                        d.rec = round - LAG;
+                        d.tile = o - TA;
+                        valid = d.rec >= 0 && d.rec < nrec;
+                    }
+                }
+                if (!valid) continue;
+                const uint32_t s = k % NSTAGE, u = k / NSTAGE;
+                P2_T(pt0)
+                if (u > 0) mbar_wait(empty0 + 8 * s, (u - 1) & 1);
+                P2_T(pt1)
+                P2_ACC(12, pt0, pt1)
+                if (d.kind == 2) {
+                    info[s] = d;
+                    mbar_arrive(full0 + 8 * s);
+                    break;
+                }
+                const int slot = (int)(d.rec % S), gen = (int)(d.rec / S);
+                if (d.kind == 0) {
+                    if (gen > 0) wait_geq(doneB + slot, gen * TB);   // ring slot free (WAR)
+                } else {
+                    wait_geq(doneA + slot, (gen + 1) * TA);          // column FFTs published
+                }
+                P2_T(pt2)
+                P2_ACC(13, pt1, pt2)
+                info[s] = d;
+                float2* stage = sm + (size_t)s * TILE;
+                const uint32_t fb = full0 + 8 * s;
+                if (d.kind == 0) {
+                    mbar_expect_tx(fb, (uint32_t)(CF::TILE_A * sizeof(float2)));
+#pragma unroll 1
+                    for (int r0 = 0; r0 < N1; r0 += CF::BOXR)
+                        tma_load_3d(smem_addr(stage + r0 * COLS), &tmap_in, d.tile * COLS, r0, (int)d.rec, fb);
+                } else {
+                    mbar_expect_tx(fb, (uint32_t)(ROWS * N2 * sizeof(float2)));
+                    const float2* src = ring + (int64_t)slot * N + (int64_t)d.tile * ROWS * N2;
+#pragma unroll 1
+                    for (int j = 0; j < ROWS; ++j)
+                        bulk_g2s(smem_addr(stage + j * RSTRIDE), src + (int64_t)j * N2, N2 * sizeof(float2), fb);
+                }
+                P2_T(pt3)
+                P2_ACC(14, pt2, pt3)
+#ifdef BFFT_PIPE_PROF
+                atomicAdd(&g_pipe_prof[15], 1ull);
+#endif
+                ++k;
+            }
+        }
+    } else if (warp == WR) {
+        // ============================================== release
+        if (lane == 0) {
+            for (uint32_t k = 0;; ++k) {
+                const uint32_t s = k % NSTAGE, u = k / NSTAGE;
+                mbar_wait(full0 + 8 * s, u & 1);
+                const PipeTask d = info[s];
+                if (d.kind == 2) break;
+                P2_T(rt0)
+                mbar_wait(done0 + 8 * s, u & 1);
+                P2_T(rt1)
+                mbar_arrive(empty0 + 8 * s);   // stage reusable (compute warps are past it)
+                fence_acq_rel_gpu();            // their stores, observed through done[s], become visible
+                const int slot = (int)(d.rec % S);
+                red_relaxed_gpu((d.kind == 0 ? doneA : doneB) + slot, 1);
+                P2_T(rt2)
+                P2_ACC(16, rt0, rt1)
+                P2_ACC(17, rt1, rt2)
+            }
+        }
+    } else {
+        // ============================================== compute warps
+        const TwoLevel W{w_hi, w_lo, w_lb, (uint32_t)(N - 1)};
+        const ConstTw<N1> tabA{};
+        const ConstTw<N2> tabB{};
+        const NamedBarrier bar{1, NTC};
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t s = k % NSTAGE, u = k / NSTAGE;
+            P2_T(ct0)
+            mbar_wait(full0 + 8 * s, u & 1);
+            P2_T(ct1)
+            const PipeTask d = info[s];
+            if (d.kind == 2) break;
+            float2* stage = sm + (size_t)s * TILE;
+            const int64_t r = d.rec;
+            const int slot = (int)(r % S);
+            float2 v[16];
+            if (d.kind == 0) {
+                // ---------------- A: columns n2 of record r, FFT over n1, twiddle, -> ring
+                const int col = tid % COLS, t = tid / COLS;
+                const int n2 = d.tile * COLS + col;
+                float2 f[4], w0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) f[i] = W((uint32_t)n2 * (uint32_t)(TA1 << i));
+                w0 = W((uint32_t)n2 * (uint32_t)t);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const float2 x = stage[(t + q * TA1) * COLS + col];
+                    v[q] = INV ? conjf2(x) : x;
+                }
+                fft_engine<N1>(v, t, stage, [&](int e) { return ColLayout<COLS>::at(e, col); }, tabA, bar);
+                float2 w[16];
+                w[0] = w0;
+                v[0] = cmul(v[0], w0);
+#pragma unroll
+                for (int q = 1; q < 16; ++q) {
+                    const int lb = (q & 1) ? 0 : (q & 2) ? 1 : (q & 4) ? 2 : 3;
+                    w[q] = cmul(w[q & (q - 1)], f[lb]);
+                    v[q] = cmul(v[q], w[q]);
+                }
+                float2* dst = ring + (int64_t)slot * N + n2 + (int64_t)t * N2;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) dst[(int64_t)q * TA1 * N2] = v[q];
+            } else {
+                // ---------------- B: rows k1 of record r, FFT over n2, -> X[k1 + N1 k2]
+                const int col = tid % ROWS, t = tid / ROWS;
+                const int k0 = d.tile * ROWS;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) v[q] = stage[col * RSTRIDE + t + q * TB2];
+                fft_engine<N2>(v, t, stage, [&](int e) { return ColLayout<ROWS>::at(e, col); }, tabB, bar);
+                float2* dst = out + r * N + k0 + col + (int64_t)t * N1;
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    st_stream(dst + (int64_t)q * TB2 * N1, INV ? scale_conj(v[q], scale) : v[q]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(done0 + 8 * s);
+            P2_T(ct2)
+            if (tid == 0) {
+                P2_ACC(18 + d.kind * 2, ct0, ct1)
+                P2_ACC(19 + d.kind * 2, ct1, ct2)
+#ifdef BFFT_PIPE_PROF
+                atomicAdd(&g_pipe_prof[22 + d.kind], 1ull);
+#endif
+            }
         }
     }
 }

@@ -246,9 +246,31 @@ static ClusterChoice pick_cluster(int log2n, int want_c, bool inv) {
 }
 
 struct PipeChoice {
-    int n1 = 0, n2 = 0, cols = 0, rows = 0;
+    int n1 = 0, n2 = 0, cols = 0, rows = 0, impl = 1, boxr = 0;
     KernelSet k;
 };
+using Pipe2Fn = void (*)(const CUtensorMap, float2*, float2*, int64_t, int*, int, int, float, const float2*,
+                         const float2*, int);
+template <int N1, int N2, int COLS, int ROWS, int NSTAGE> static PipeChoice pipe2_kernel(bool inv) {
+    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE>;
+    PipeChoice ch;
+    ch.n1 = N1;
+    ch.n2 = N2;
+    ch.cols = COLS;
+    ch.rows = ROWS;
+    ch.impl = 2;
+    ch.boxr = CF::BOXR;
+    ch.k.fn = inv ? (const void*)&k_pipe2<N1, N2, COLS, ROWS, true, NSTAGE>
+                  : (const void*)&k_pipe2<N1, N2, COLS, ROWS, false, NSTAGE>;
+    ch.k.threads = CF::NT;
+    ch.k.smem = CF::SMEM;
+    return ch;
+}
+template <int N1, int N2, int COLS, int ROWS> static PipeChoice pipe2_pick(bool inv) {
+    int ns = 2;
+    if (const char* e = getenv("BLOCKFFT_PIPE_STAGES")) ns = atoi(e);
+    return ns == 3 ? pipe2_kernel<N1, N2, COLS, ROWS, 3>(inv) : pipe2_kernel<N1, N2, COLS, ROWS, 2>(inv);
+}
 template <int N1, int N2, int COLS, int ROWS> static PipeChoice pipe_kernel(bool inv) {
     using CF = PipeCfg<N1, N2, COLS, ROWS>;
     PipeChoice ch;
@@ -263,6 +285,23 @@ template <int N1, int N2, int COLS, int ROWS> static PipeChoice pipe_kernel(bool
 }
 // Pipelined four-step splits (N1 >= N2; A-tile COLS columns, B-tile ROWS rows).
 static PipeChoice pick_pipe(int log2n, bool inv) {
+    // fastest measured per size (profiles/r01_variants_*): warp-specialised
+    // k_pipe2 for 2^15 and 2^18..2^20, k_pipe otherwise (k_pipe2 also needs
+    // NTC + 64 <= 1024 threads, so not 2^21..2^22)
+    int impl = (log2n == 15 || (log2n >= 18 && log2n <= 20)) ? 2 : 1;
+    if (const char* e = getenv("BLOCKFFT_PIPE_IMPL")) impl = atoi(e);
+    if (impl == 2) {
+        switch (log2n) {
+            case 14: return pipe2_pick<128, 128, 16, 16>(inv);
+            case 15: return pipe2_pick<256, 128, 16, 32>(inv);
+            case 16: return pipe2_pick<256, 256, 16, 16>(inv);
+            case 17: return pipe2_pick<512, 256, 16, 32>(inv);
+            case 18: return pipe2_pick<512, 512, 16, 16>(inv);
+            case 19: return pipe2_pick<1024, 512, 8, 16>(inv);
+            case 20: return pipe2_pick<1024, 1024, 8, 8>(inv);
+            default: return PipeChoice{};
+        }
+    }
     switch (log2n) {
         case 14: return pipe_kernel<128, 128, 16, 16>(inv);
         case 15: return pipe_kernel<256, 128, 32, 64>(inv);
@@ -366,6 +405,7 @@ struct fft_plan {
     int n1 = 0, n2 = 0, cluster = 1, cluster_impl = 0;
     int pipe_S = 0, pipe_LAG = 0;     // pipelined four-step ring depth and lag
     int w_lb = 0;                     // two-level twiddle split (tw_a = hi, tw_b = lo)
+    int pipe_impl = 1, pipe_boxr = 0; // k_pipe (1) or warp-specialised k_pipe2 (2)
     int* d_ctr = nullptr;             // pipelined four-step task/dependency counters
     float scale = 1.f;
     float2* d_tab = nullptr;          // all twiddle tables
@@ -458,6 +498,8 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         p->n2 = ch.n2;
         p->ka.cols = ch.cols;
         p->kb.cols = ch.rows;
+        p->pipe_impl = ch.impl;
+        p->pipe_boxr = ch.boxr;
         // two-level W_N table: hi[a] = W_N^{a 2^lb}, lo[b] = W_N^b (fp64 -> fp32)
         p->w_lb = (p->log2n + 1) / 2;
         const int nhi = 1 << (p->log2n - p->w_lb), nlo = 1 << p->w_lb;
@@ -669,9 +711,18 @@ static int launch(const fft_plan* p, const float2* in, float2* out, int64_t coun
         case FFT_VARIANT_PIPE: {
             CUDA_TRY(cudaMemsetAsync(p->d_ctr, 0, sizeof(int) * (1 + 2 * p->pipe_S), st));
             const int grid = p->occ_a * p->sms;
-            ((PipeFn)p->ka.fn)<<<grid, p->ka.threads, p->ka.smem, st>>>(in, out, p->d_scratch, count, p->d_ctr,
-                                                                       p->pipe_S, p->pipe_LAG, p->scale, p->tw_a,
-                                                                       p->tw_b, p->w_lb);
+            if (p->pipe_impl == 2) {
+                CUtensorMap tm;
+                int rc = make_record_tmap(&tm, in, count, p->n1, p->n2, p->ka.cols, p->pipe_boxr);
+                if (rc) return rc;
+                ((Pipe2Fn)p->ka.fn)<<<grid, p->ka.threads, p->ka.smem, st>>>(tm, out, p->d_scratch, count, p->d_ctr,
+                                                                            p->pipe_S, p->pipe_LAG, p->scale, p->tw_a,
+                                                                            p->tw_b, p->w_lb);
+            } else {
+                ((PipeFn)p->ka.fn)<<<grid, p->ka.threads, p->ka.smem, st>>>(in, out, p->d_scratch, count, p->d_ctr,
+                                                                           p->pipe_S, p->pipe_LAG, p->scale, p->tw_a,
+                                                                           p->tw_b, p->w_lb);
+            }
             break;
         }
         case FFT_VARIANT_FOURSTEP: {
