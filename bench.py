@@ -122,13 +122,21 @@ def ncu_traffic(kernel_substr, n, batch):
 
 
 # ------------------------------------------------------------------ oracle arm
+def host_cores():
+    """Host cores available to this process (torchrun sets OMP_NUM_THREADS=1
+    per rank, so the OpenMP default is not the machine)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def oracle_rate(n, seconds=10.0, threads=0, min_records=None):
     """Time the CPU oracle (as it stands) on a bounded sample of records of
     length n, all host cores; returns (records/s, cores, sample description)."""
-    import numpy as np
     import oracle
     import synth
-    cores = oracle.max_threads() if threads <= 0 else threads
+    cores = host_cores() if threads <= 0 else threads
     per = max(cores, 1) if min_records is None else min_records
     x = synth.random_records(synth.DEFAULT_SEED, n, 0, per)
     done, t0 = 0, time.perf_counter()
@@ -147,7 +155,7 @@ def run_reference(args, cfg):
         return 0
     n = cfg["n"]
     import oracle
-    cores = oracle.max_threads()
+    cores = host_cores()
     steps = []
     per_step = max(cores, 8)
     import synth
