@@ -246,7 +246,7 @@ static ClusterChoice pick_cluster(int log2n, int want_c, bool inv) {
 }
 
 struct PipeChoice {
-    int n1 = 0, n2 = 0, cols = 0, rows = 0, impl = 1, boxr = 0;
+    int n1 = 0, n2 = 0, cols = 0, rows = 0, impl = 1, boxr = 0, stages = 0;
     KernelSet k;
 };
 using Pipe2Fn = void (*)(const CUtensorMap, float2*, float2*, int64_t, int*, int, int, float, const float2*,
@@ -259,6 +259,7 @@ template <int N1, int N2, int COLS, int ROWS, int NSTAGE> static PipeChoice pipe
     ch.cols = COLS;
     ch.rows = ROWS;
     ch.impl = 2;
+    ch.stages = NSTAGE;
     ch.boxr = CF::BOXR;
     ch.k.fn = inv ? (const void*)&k_pipe2<N1, N2, COLS, ROWS, true, NSTAGE>
                   : (const void*)&k_pipe2<N1, N2, COLS, ROWS, false, NSTAGE>;
@@ -288,7 +289,7 @@ static PipeChoice pick_pipe(int log2n, bool inv) {
     // fastest measured per size (profiles/r01_variants_*): warp-specialised
     // k_pipe2 for 2^15 and 2^18..2^20, k_pipe otherwise (k_pipe2 also needs
     // NTC + 64 <= 1024 threads, so not 2^21..2^22)
-    int impl = (log2n == 15 || (log2n >= 18 && log2n <= 20)) ? 2 : 1;
+    int impl = (log2n >= 15 && log2n <= 20) ? 2 : 1;
     if (const char* e = getenv("BLOCKFFT_PIPE_IMPL")) impl = atoi(e);
     if (impl == 2) {
         switch (log2n) {
@@ -575,15 +576,23 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         p->occ_a = std::max(p->occ_a, 1);
         const int resident = p->occ_a * p->sms;
         const int per_round = p->n2 / p->ka.cols + p->n1 / p->kb.cols;
-        // B-tasks of record r are issued LAG rounds after its A-tasks and an
-        // A-task reuses the slot of record r - S, whose B-tasks were issued
-        // S - LAG rounds earlier: both gaps span ~2 x the resident CTAs, so
-        // dependencies are normally complete when a task starts.  The ring is
-        // capped at 96 MiB to stay resident in the 126 MB L2.
-        p->pipe_LAG = (2 * resident + per_round - 1) / per_round + 1;
+        PipeChoice ch = pick_pipe(p->log2n, inv);
+        // B-tasks of record r are issued LAG rounds after its A-tasks, and an
+        // A-task reuses the ring slot of record r - S, whose B-tasks were
+        // issued S - LAG rounds earlier.  Both gaps must exceed the tasks a
+        // GPU holds in flight (resident CTAs x tasks each CTA has claimed:
+        // 1 for k_pipe, stages + 1 for k_pipe2) or tasks stall on their
+        // dependencies; measured best on B200 (profiles/r01_pipe_lag_sweep.txt):
+        // LAG ~ 1.5x and S - LAG ~ 2x the in-flight rounds.  The ring is capped
+        // at 96 MiB so it stays resident in the 126 MB L2.
+        const int stages = ch.impl == 2 ? ch.stages : 0;
+        const int64_t inflight = (int64_t)resident * (stages + 1);
+        const int64_t rounds = (inflight + per_round - 1) / per_round;
+        p->pipe_LAG = (int)(3 * rounds / 2 + 1);
+        if (const char* e = getenv("BLOCKFFT_PIPE_LAG")) p->pipe_LAG = std::max(1, atoi(e));
         const int64_t rec_bytes = n * (int64_t)sizeof(float2);
         const int s_cap = (int)std::max<int64_t>(p->pipe_LAG + 2, (96ll << 20) / rec_bytes);
-        p->pipe_S = std::min(2 * p->pipe_LAG + 1, s_cap);
+        p->pipe_S = (int)std::min<int64_t>(p->pipe_LAG + 2 * rounds + 1, s_cap);
         if (const char* e = getenv("BLOCKFFT_PIPE_S")) p->pipe_S = std::max(p->pipe_LAG + 1, atoi(e));
         const size_t rb = (size_t)p->pipe_S * (size_t)n * sizeof(float2);
         cudaError_t e = cudaMalloc(&p->d_scratch, rb);

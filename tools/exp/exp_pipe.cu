@@ -4,8 +4,8 @@
 using namespace bfft;
 extern "C" int exp_pipe(const void* in, void* out, void* ring, int* ctr, long long nrec, int S, int LAG,
                         const void* hi, const void* lo, int lb, unsigned long long* prof, float* ms) {
-    auto fn = k_pipe<256, 256, 32, 32, false>;
-    using CF = PipeCfg<256, 256, 32, 32>;
+    auto fn = k_pipe<256, 256, 16, 16, false>;
+    using CF = PipeCfg<256, 256, 16, 16>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, CF::NT, CF::SMEM);
