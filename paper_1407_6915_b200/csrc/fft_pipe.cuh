@@ -39,6 +39,26 @@ __device__ __forceinline__ void wait_geq(const int* p, int target) {
     }
 }
 __device__ __forceinline__ float2 ld_l2(const float2* p) { return __ldcg(p); }
+// Drop a dead 128-byte line of the ring from L2 without writing it back: once
+// a B-task holds its rows in shared memory the intermediate is dead, and
+// discarding it keeps the ring's dirty lines from ever reaching HBM.
+__device__ __forceinline__ void l2_discard128(const void* p) {
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+// L2 eviction-priority policy for streaming data read exactly once.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_load_3d_hint(uint32_t dst, const CUtensorMap* tmap, int c0, int c1, int c2,
+                                                 uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+        "{%2, %3, %4}], [%5], %6;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(pol)
+        : "memory");
+}
 
 // W_N^m from the plan's two-level table (fp64-computed, fp32-rounded):
 // W^m = hi[m >> LB] * lo[m & (2^LB - 1)], one extra rounding.
@@ -194,6 +214,8 @@ k_pipe(const float2* __restrict__ in, float2* __restrict__ out, float2* __restri
                 sm[SwzColLayout<ROWS>::at(e, row)] = ld_l2(src + i);
             }
             __syncthreads();
+            for (int i = tid; i < ROWS * N2 * 8 / 128; i += NT)
+                l2_discard128(reinterpret_cast<const char*>(src) + 128 * i);  // dead intermediate: no write-back
             if (tid == 0) red_release_gpu(doneB + slot, 1);  // slot rows read: A-tasks may reuse
             PIPE_T(6)
             const int col = tid % ROWS, t = tid / ROWS;
@@ -302,6 +324,7 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
         // ============================================== producer
         if (lane == 0) {
             uint32_t k = 0;
+            const uint64_t pol_stream = policy_evict_first();
             // the claim of the next task is in flight while this one is staged
             long long next = atomicAdd(ctr, 1);
             for (;;) {
@@ -354,7 +377,8 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                     mbar_expect_tx(fb, (uint32_t)(CF::TILE_A * sizeof(float2)));
 #pragma unroll 1
                     for (int r0 = 0; r0 < N1; r0 += CF::BOXR)
-                        tma_load_3d(smem_addr(stage + r0 * COLS), &tmap_in, d.tile * COLS, r0, (int)d.rec, fb);
+                        tma_load_3d_hint(smem_addr(stage + r0 * COLS), &tmap_in, d.tile * COLS, r0, (int)d.rec, fb,
+                                         pol_stream);
                 } else {
                     mbar_expect_tx(fb, (uint32_t)(ROWS * N2 * sizeof(float2)));
                     const float2* src = ring + (int64_t)slot * N + (int64_t)d.tile * ROWS * N2;
@@ -437,6 +461,10 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 // ---------------- B: rows k1 of record r, FFT over n2, -> X[k1 + N1 k2]
                 const int col = tid % ROWS, t = tid / ROWS;
                 const int k0 = d.tile * ROWS;
+                {   // the tile's ring rows are staged: drop them from L2 (no write-back)
+                    const char* rows = reinterpret_cast<const char*>(ring + (int64_t)slot * N + (int64_t)k0 * N2);
+                    for (int i = tid; i < ROWS * N2 * 8 / 128; i += NTC) l2_discard128(rows + 128 * i);
+                }
 #pragma unroll
                 for (int q = 0; q < 16; ++q) v[q] = stage[col * RSTRIDE + t + q * TB2];
                 fft_engine<N2>(v, t, stage, [&](int e) { return ColLayout<ROWS>::at(e, col); }, tabB, bar);

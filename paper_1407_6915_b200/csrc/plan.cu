@@ -289,7 +289,7 @@ static PipeChoice pick_pipe(int log2n, bool inv) {
     // fastest measured per size (profiles/r01_variants_*): warp-specialised
     // k_pipe2 for 2^15 and 2^18..2^20, k_pipe otherwise (k_pipe2 also needs
     // NTC + 64 <= 1024 threads, so not 2^21..2^22)
-    int impl = (log2n >= 15 && log2n <= 20) ? 2 : 1;
+    int impl = (log2n >= 14 && log2n <= 20) ? 2 : 1;
     if (const char* e = getenv("BLOCKFFT_PIPE_IMPL")) impl = atoi(e);
     if (impl == 2) {
         switch (log2n) {

@@ -9,7 +9,7 @@ x = torch.randn((b, n), dtype=torch.complex64, device="cuda"); y = torch.empty_l
 lb = 8
 hi = torch.tensor([complex(math.cos(-2*math.pi*(a<<lb)/n), math.sin(-2*math.pi*(a<<lb)/n)) for a in range(n >> lb)], dtype=torch.complex64, device="cuda")
 lo = torch.tensor([complex(math.cos(-2*math.pi*k/n), math.sin(-2*math.pi*k/n)) for k in range(1 << lb)], dtype=torch.complex64, device="cuda")
-for S, LAG in ((81, 40), (81, 40), (161, 80)):
+for S, LAG in ((140, 60), (121, 60), (124, 55)):
     ring = torch.empty((S, n), dtype=torch.complex64, device="cuda")
     ctr = torch.zeros(1 + 2 * S, dtype=torch.int32, device="cuda")
     prof = (ctypes.c_ulonglong * 32)(); ms = ctypes.c_float()
