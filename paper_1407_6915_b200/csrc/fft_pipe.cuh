@@ -35,7 +35,7 @@ __device__ __forceinline__ void wait_geq(const int* p, int target) {
     int ns = 32;
     while (ld_acquire_gpu(p) < target) {
         __nanosleep(ns);
-        ns = ns < 1024 ? 2 * ns : ns;
+        ns = ns < 256 ? 2 * ns : ns;
     }
 }
 __device__ __forceinline__ float2 ld_l2(const float2* p) { return __ldcg(p); }
@@ -322,16 +322,18 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
 
     if (warp == WP) {
         // ============================================== producer
-        if (lane == 0) {
-            uint32_t k = 0;
-            const uint64_t pol_stream = policy_evict_first();
-            // the claim of the next task is in flight while this one is staged
-            long long next = atomicAdd(ctr, 1);
-            for (;;) {
+        // lane 0 claims, waits and arms the stage; the B-tile's ROWS row copies
+        // are spread over the warp's lanes
+        uint32_t k = 0;
+        const uint64_t pol_stream = policy_evict_first();
+        long long next = 0;
+        if (lane == 0) next = atomicAdd(ctr, 1);  // the next claim is in flight while a task is staged
+        for (;;) {
+            PipeTask d;
+            bool valid = true;
+            if (lane == 0) {
                 const long long task = next;
                 if (task < total) next = atomicAdd(ctr, 1);
-                PipeTask d;
-                bool valid = true;
                 if (task >= total) {
                     d.kind = 2;
                     d.rec = 0;
@@ -351,48 +353,47 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                         valid = d.rec >= 0 && d.rec < nrec;
                     }
                 }
-                if (!valid) continue;
-                const uint32_t s = k % NSTAGE, u = k / NSTAGE;
-                P2_T(pt0)
+            }
+            valid = __shfl_sync(0xffffffffu, valid, 0);
+            if (!valid) continue;
+            d.kind = __shfl_sync(0xffffffffu, d.kind, 0);
+            d.rec = __shfl_sync(0xffffffffu, d.rec, 0);
+            d.tile = __shfl_sync(0xffffffffu, d.tile, 0);
+            const uint32_t s = k % NSTAGE, u = k / NSTAGE;
+            const uint32_t fb = full0 + 8 * s;
+            if (lane == 0) {
                 if (u > 0) mbar_wait(empty0 + 8 * s, (u - 1) & 1);
-                P2_T(pt1)
-                P2_ACC(12, pt0, pt1)
                 if (d.kind == 2) {
                     info[s] = d;
-                    mbar_arrive(full0 + 8 * s);
-                    break;
-                }
-                const int slot = (int)(d.rec % S), gen = (int)(d.rec / S);
-                if (d.kind == 0) {
-                    if (gen > 0) wait_geq(doneB + slot, gen * TB);   // ring slot free (WAR)
+                    mbar_arrive(fb);
                 } else {
-                    wait_geq(doneA + slot, (gen + 1) * TA);          // column FFTs published
+                    const int slot = (int)(d.rec % S), gen = (int)(d.rec / S);
+                    if (d.kind == 0) {
+                        if (gen > 0) wait_geq(doneB + slot, gen * TB);   // ring slot free (WAR)
+                    } else {
+                        wait_geq(doneA + slot, (gen + 1) * TA);          // column FFTs published
+                    }
+                    info[s] = d;
+                    mbar_expect_tx(fb, (uint32_t)((d.kind == 0 ? CF::TILE_A : ROWS * N2) * sizeof(float2)));
                 }
-                P2_T(pt2)
-                P2_ACC(13, pt1, pt2)
-                info[s] = d;
-                float2* stage = sm + (size_t)s * TILE;
-                const uint32_t fb = full0 + 8 * s;
-                if (d.kind == 0) {
-                    mbar_expect_tx(fb, (uint32_t)(CF::TILE_A * sizeof(float2)));
+            }
+            if (d.kind == 2) break;
+            __syncwarp();
+            float2* stage = sm + (size_t)s * TILE;
+            if (d.kind == 0) {
+                if (lane == 0) {
 #pragma unroll 1
                     for (int r0 = 0; r0 < N1; r0 += CF::BOXR)
                         tma_load_3d_hint(smem_addr(stage + r0 * COLS), &tmap_in, d.tile * COLS, r0, (int)d.rec, fb,
                                          pol_stream);
-                } else {
-                    mbar_expect_tx(fb, (uint32_t)(ROWS * N2 * sizeof(float2)));
-                    const float2* src = ring + (int64_t)slot * N + (int64_t)d.tile * ROWS * N2;
-#pragma unroll 1
-                    for (int j = 0; j < ROWS; ++j)
-                        bulk_g2s(smem_addr(stage + j * RSTRIDE), src + (int64_t)j * N2, N2 * sizeof(float2), fb);
                 }
-                P2_T(pt3)
-                P2_ACC(14, pt2, pt3)
-#ifdef BFFT_PIPE_PROF
-                atomicAdd(&g_pipe_prof[15], 1ull);
-#endif
-                ++k;
+            } else {
+                const int slot = (int)(d.rec % S);
+                const float2* src = ring + (int64_t)slot * N + (int64_t)d.tile * ROWS * N2;
+                for (int j = lane; j < ROWS; j += 32)
+                    bulk_g2s(smem_addr(stage + j * RSTRIDE), src + (int64_t)j * N2, N2 * sizeof(float2), fb);
             }
+            ++k;
         }
     } else if (warp == WR) {
         // ============================================== release

@@ -289,15 +289,20 @@ static PipeChoice pick_pipe(int log2n, bool inv) {
     // fastest measured per size (profiles/r01_variants_*): warp-specialised
     // k_pipe2 for 2^15 and 2^18..2^20, k_pipe otherwise (k_pipe2 also needs
     // NTC + 64 <= 1024 threads, so not 2^21..2^22)
-    int impl = (log2n >= 14 && log2n <= 20) ? 2 : 1;
+    int impl = (log2n >= 13 && log2n <= 20) ? 2 : 1;
     if (const char* e = getenv("BLOCKFFT_PIPE_IMPL")) impl = atoi(e);
     if (impl == 2) {
         switch (log2n) {
+            case 13: return pipe2_pick<128, 64, 16, 32>(inv);
             case 14: return pipe2_pick<128, 128, 16, 16>(inv);
             case 15: return pipe2_pick<256, 128, 16, 32>(inv);
             case 16: return pipe2_pick<256, 256, 16, 16>(inv);
-            case 17: return pipe2_pick<512, 256, 16, 32>(inv);
-            case 18: return pipe2_pick<512, 512, 16, 16>(inv);
+            case 17:
+                if (getenv("BLOCKFFT_PIPE_WIDE")) return pipe2_pick<512, 256, 16, 32>(inv);
+                return pipe2_pick<512, 256, 8, 16>(inv);
+            case 18:
+                if (getenv("BLOCKFFT_PIPE_WIDE")) return pipe2_pick<512, 512, 16, 16>(inv);
+                return pipe2_pick<512, 512, 8, 8>(inv);
             case 19: return pipe2_pick<1024, 512, 8, 16>(inv);
             case 20: return pipe2_pick<1024, 1024, 8, 8>(inv);
             default: return PipeChoice{};
@@ -436,7 +441,6 @@ static int default_variant(int log2n) {
     }
     // fastest measured per size (profiles/r01_variants_*.txt)
     if (log2n <= 12) return FFT_VARIANT_SINGLE;
-    if (log2n == 13) return FFT_VARIANT_CLUSTER;
     return FFT_VARIANT_PIPE;
 }
 

@@ -85,7 +85,7 @@ def test_fourstep(n, direction):
     check(x, direction, bf.VARIANT_FOURSTEP)
 
 
-PIPE = [2 ** k for k in range(14, 23)]
+PIPE = [2 ** k for k in range(13, 23)]
 
 
 @pytest.mark.parametrize("direction", [-1, 1])
