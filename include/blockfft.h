@@ -207,6 +207,12 @@ int fft_file_ex(const char *in_path, const char *out_path, int64_t record_len, i
 int fft_exec_host(int64_t n, int64_t batch, int dir, const void *host_in, void *host_out,
                   int device, const fft_stream_opts *opts, fft_stream_stats *stats);
 
+/* The streamer (fft_file*, fft_exec_host) caches its per-GPU resources
+ * (plan, streams, device slots, pinned staging) between calls, keyed by
+ * (device, n, dir, variant, chunk records, depth); fft_stream_release frees
+ * every cached set not in use and returns how many it freed.              */
+int fft_stream_release(void);
+
 /* Thread-local message describing the last error on this thread ("" if none). */
 const char *fft_last_error(void);
 

@@ -167,6 +167,11 @@ def exec_host(x_host, n: int, direction: int = FFT_FORWARD, device: int = 0, out
     return st.as_dict()
 
 
+def stream_release() -> int:
+    """Free the streamer's cached per-GPU resources (fft_stream_release)."""
+    return int(_lib.fft_stream_release())
+
+
 def _host_ptr(a):
     try:
         import torch

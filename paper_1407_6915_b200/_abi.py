@@ -27,7 +27,7 @@ VARIANT_NAMES = {0: "auto", 1: "single", 2: "cluster", 3: "fourstep", 4: "identi
 # Every symbol include/blockfft.h declares (checked by tests/test_abi.py).
 EXPORTED = ["fft_plan_create", "fft_plan_create_ex", "fft_exec", "fft_exec_range",
             "fft_plan_destroy", "fft_plan_get_info", "fft_file_records", "fft_partition",
-            "fft_file", "fft_file_ex", "fft_exec_host", "fft_last_error", "fft_last_status", "fft_version"]
+            "fft_file", "fft_file_ex", "fft_exec_host", "fft_stream_release", "fft_last_error", "fft_last_status", "fft_version"]
 
 
 class PlanInfo(ctypes.Structure):
@@ -76,6 +76,7 @@ def load() -> ctypes.CDLL:
                               ctypes.POINTER(StreamOpts), ctypes.POINTER(StreamStats)]),
         "fft_exec_host": (i32, [i64, i64, i32, vp, vp, i32, ctypes.POINTER(StreamOpts),
                                 ctypes.POINTER(StreamStats)]),
+        "fft_stream_release": (i32, []),
         "fft_last_error": (ctypes.c_char_p, []),
         "fft_last_status": (i32, []),
         "fft_version": (i32, []),

@@ -167,14 +167,6 @@ struct Stats {
     }
 };
 
-#define CK(call)                                                                                    \
-    do {                                                                                            \
-        cudaError_t e_ = (call);                                                                    \
-        if (e_ != cudaSuccess) {                                                                    \
-            rc = bfft_set_error(FFT_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));        \
-            goto done;                                                                              \
-        }                                                                                           \
-    } while (0)
 
 struct Opts {
     int64_t chunk_bytes = 256ll << 20;
@@ -193,36 +185,162 @@ Opts resolve(const fft_stream_opts* o) {
     return r;
 }
 
+// Per-GPU pipeline resources (plan, streams, events, device slots, pinned
+// staging), cached across calls: allocating and freeing hundreds of MiB of
+// device and pinned memory per call costs tens of ms and synchronises the
+// device.  A context is used by one call at a time; fft_stream_release()
+// frees every idle context.
+struct StreamCtx {
+    int device = 0, dir = 0, variant = 0, depth = 0;
+    int64_t n = 0, crec = 0;
+    bool staging = false, busy = false;
+    fft_plan* plan = nullptr;
+    cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
+    std::vector<cudaEvent_t> e0, e1, e2, e3;
+    std::vector<void*> dbuf, hbuf;
+    void release() {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(device);
+        if (sh) cudaStreamSynchronize(sh);
+        if (sc) cudaStreamSynchronize(sc);
+        if (sd) cudaStreamSynchronize(sd);
+        for (auto* v : {&e0, &e1, &e2, &e3})
+            for (auto ev : *v)
+                if (ev) cudaEventDestroy(ev);
+        for (void* b : dbuf)
+            if (b) cudaFree(b);
+        for (void* b : hbuf)
+            if (b) cudaFreeHost(b);
+        if (sh) cudaStreamDestroy(sh);
+        if (sc) cudaStreamDestroy(sc);
+        if (sd) cudaStreamDestroy(sd);
+        fft_plan_destroy(plan);
+        cudaSetDevice(cur);
+    }
+};
+
+std::mutex g_ctx_mu;
+std::vector<StreamCtx*> g_ctx;
+
+#define CKC(call)                                                                                   \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess) {                                                                    \
+            int rc_ = bfft_set_error(FFT_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));   \
+            c->release();                                                                           \
+            delete c;                                                                               \
+            *out = nullptr;                                                                         \
+            return rc_;                                                                             \
+        }                                                                                           \
+    } while (0)
+
+int acquire_ctx(int device, int64_t n, int dir, int variant, int64_t crec, int D, bool staging, StreamCtx** out) {
+    {
+        std::lock_guard<std::mutex> g(g_ctx_mu);
+        for (StreamCtx* c : g_ctx)
+            if (!c->busy && c->device == device && c->n == n && c->dir == dir && c->variant == variant &&
+                c->crec == crec && c->depth == D && c->staging == staging) {
+                c->busy = true;
+                *out = c;
+                return FFT_OK;
+            }
+    }
+    StreamCtx* c = new StreamCtx();
+    *out = c;
+    c->device = device;
+    c->n = n;
+    c->dir = dir;
+    c->variant = variant;
+    c->crec = crec;
+    c->depth = D;
+    c->staging = staging;
+    c->busy = true;
+    CKC(cudaSetDevice(device));
+    c->plan = fft_plan_create_ex(n, crec, dir, dir == 0 ? FFT_VARIANT_IDENTITY : variant);
+    if (!c->plan) {
+        const int code = bfft_last_code();
+        delete c;
+        *out = nullptr;
+        return code;  // message already set by the plan layer
+    }
+    CKC(cudaStreamCreateWithFlags(&c->sh, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&c->sc, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&c->sd, cudaStreamNonBlocking));
+    for (auto* v : {&c->e0, &c->e1, &c->e2, &c->e3}) {
+        v->assign(D, nullptr);
+        for (int i = 0; i < D; ++i) CKC(cudaEventCreate(&(*v)[i]));
+    }
+    c->dbuf.assign(D, nullptr);
+    c->hbuf.assign(D, nullptr);
+    const size_t bytes = (size_t)(crec * 8 * n);
+    for (int i = 0; i < D; ++i) {
+        cudaError_t e = cudaMalloc(&c->dbuf[i], bytes);
+        if (e != cudaSuccess) {
+            int rc = bfft_set_error(FFT_E_NOMEM, "cudaMalloc(%zu) for stream slot failed: %s", bytes, cudaGetErrorString(e));
+            c->release();
+            delete c;
+            *out = nullptr;
+            return rc;
+        }
+        if (staging) {
+            e = cudaHostAlloc(&c->hbuf[i], bytes, cudaHostAllocPortable);
+            if (e != cudaSuccess) {
+                int rc = bfft_set_error(FFT_E_NOMEM, "cudaHostAlloc(%zu) for stream slot failed: %s", bytes, cudaGetErrorString(e));
+                c->release();
+                delete c;
+                *out = nullptr;
+                return rc;
+            }
+        }
+    }
+    std::lock_guard<std::mutex> g(g_ctx_mu);
+    g_ctx.push_back(c);
+    return FFT_OK;
+}
+
+void release_ctx(StreamCtx* c, bool broken) {
+    std::lock_guard<std::mutex> g(g_ctx_mu);
+    if (broken) {  // a failed pipeline may leave work queued: do not reuse it
+        for (size_t i = 0; i < g_ctx.size(); ++i)
+            if (g_ctx[i] == c) {
+                g_ctx.erase(g_ctx.begin() + (long)i);
+                break;
+            }
+        c->release();
+        delete c;
+        return;
+    }
+    c->busy = false;
+}
+
 // The per-GPU pipeline over records [first, first+count).
 int run_pipeline(int device, int64_t n, int dir, int64_t first, int64_t count, Source* src, Sink* dst,
                  const Opts& o, fft_stream_stats* st) {
-    int rc = FFT_OK;
     const int64_t rb = 8 * n;
     const int64_t crec = std::max<int64_t>(1, std::min<int64_t>(count, o.chunk_bytes / rb));
     const int D = o.depth;
-    std::vector<void*> hbuf(D, nullptr), dbuf(D, nullptr);
-    std::vector<cudaEvent_t> e0(D), e1(D), e2(D), e3(D);
+    const bool staging = !src->direct(first) || !dst->direct(first);
+    StreamCtx* c = nullptr;
+    int rc = acquire_ctx(device, n, dir, o.variant, crec, D, staging, &c);
+    if (rc) return rc;
     std::vector<int64_t> slot_first(D, -1), slot_count(D, 0);
-    std::vector<double> slot_t(D, 0);
-    cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
-    fft_plan* plan = nullptr;
-    bool ev_made = false;
     const int64_t nchunks = (count + crec - 1) / crec;
     auto retire = [&](int i) -> int {
         // wait for slot i's D2H, account its times, hand its output to the sink
         if (slot_first[i] < 0) return FFT_OK;
-        cudaError_t e = cudaEventSynchronize(e3[i]);
+        cudaError_t e = cudaEventSynchronize(c->e3[i]);
         if (e != cudaSuccess) return bfft_set_error(FFT_E_CUDA, "pipeline failed: %s", cudaGetErrorString(e));
-        float a = 0, b = 0, c = 0;
-        cudaEventElapsedTime(&a, e0[i], e1[i]);
-        cudaEventElapsedTime(&b, e1[i], e2[i]);
-        cudaEventElapsedTime(&c, e2[i], e3[i]);
+        float a = 0, b = 0, cc = 0;
+        cudaEventElapsedTime(&a, c->e0[i], c->e1[i]);
+        cudaEventElapsedTime(&b, c->e1[i], c->e2[i]);
+        cudaEventElapsedTime(&cc, c->e2[i], c->e3[i]);
         st->h2d_s += a * 1e-3;
         st->fft_s += b * 1e-3;
-        st->d2h_s += c * 1e-3;
+        st->d2h_s += cc * 1e-3;
         if (!dst->direct(slot_first[i])) {
             double t0 = now_s();
-            int r = dst->write(slot_first[i], slot_count[i], hbuf[i]);
+            int r = dst->write(slot_first[i], slot_count[i], c->hbuf[i]);
             st->write_s += now_s() - t0;
             if (r) return r;
         }
@@ -230,82 +348,53 @@ int run_pipeline(int device, int64_t n, int dir, int64_t first, int64_t count, S
         slot_first[i] = -1;
         return FFT_OK;
     };
-
-    CK(cudaSetDevice(device));
-    plan = fft_plan_create_ex(n, crec, dir, dir == 0 ? FFT_VARIANT_IDENTITY : o.variant);
-    if (!plan) return bfft_last_code();  // message already set by the plan layer
-    CK(cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
-    for (int i = 0; i < D; ++i) {
-        CK(cudaEventCreate(&e0[i]));
-        CK(cudaEventCreate(&e1[i]));
-        CK(cudaEventCreate(&e2[i]));
-        CK(cudaEventCreate(&e3[i]));
-    }
-    ev_made = true;
-    for (int i = 0; i < D && i < nchunks; ++i) {
-        cudaError_t e = cudaMalloc(&dbuf[i], (size_t)(crec * rb));
-        if (e != cudaSuccess) { rc = bfft_set_error(FFT_E_NOMEM, "cudaMalloc(%lld) for stream slot failed: %s", (long long)(crec * rb), cudaGetErrorString(e)); goto done; }
-        if (!src->direct(first) || !dst->direct(first)) {
-            e = cudaHostAlloc(&hbuf[i], (size_t)(crec * rb), cudaHostAllocPortable);
-            if (e != cudaSuccess) { rc = bfft_set_error(FFT_E_NOMEM, "cudaHostAlloc(%lld) for stream slot failed: %s", (long long)(crec * rb), cudaGetErrorString(e)); goto done; }
-        }
-    }
-    for (int64_t c = 0; c < nchunks; ++c) {
-        const int i = (int)(c % D);
+    cudaError_t ce = cudaSetDevice(device);
+    if (ce != cudaSuccess) rc = bfft_set_error(FFT_E_CUDA, "cudaSetDevice(%d) failed: %s", device, cudaGetErrorString(ce));
+    for (int64_t k = 0; rc == FFT_OK && k < nchunks; ++k) {
+        const int i = (int)(k % D);
         rc = retire(i);
-        if (rc) goto done;
-        const int64_t f = first + c * crec;
-        const int64_t k = std::min<int64_t>(crec, first + count - f);
+        if (rc) break;
+        const int64_t f = first + k * crec;
+        const int64_t cnt = std::min<int64_t>(crec, first + count - f);
         const void* hin = src->direct(f);
         if (!hin) {
             double t0 = now_s();
-            rc = src->read(f, k, hbuf[i]);
+            rc = src->read(f, cnt, c->hbuf[i]);
             st->read_s += now_s() - t0;
-            if (rc) goto done;
-            hin = hbuf[i];
+            if (rc) break;
+            hin = c->hbuf[i];
         }
         void* hout = dst->direct(f);
-        if (!hout) hout = hbuf[i];
-        CK(cudaEventRecord(e0[i], sh));
-        CK(cudaMemcpyAsync(dbuf[i], hin, (size_t)(k * rb), cudaMemcpyHostToDevice, sh));
-        CK(cudaEventRecord(e1[i], sh));
-        CK(cudaStreamWaitEvent(sc, e1[i], 0));
-        rc = fft_exec_range(plan, dbuf[i], dbuf[i], k, sc);
-        if (rc) goto done;
-        CK(cudaEventRecord(e2[i], sc));
-        CK(cudaStreamWaitEvent(sd, e2[i], 0));
-        CK(cudaMemcpyAsync(hout, dbuf[i], (size_t)(k * rb), cudaMemcpyDeviceToHost, sd));
-        CK(cudaEventRecord(e3[i], sd));
-        slot_first[i] = f;
-        slot_count[i] = k;
-        st->records += k;
-        st->chunks += 1;
-        st->bytes_in += k * rb;
-    }
-    for (int64_t c = nchunks; c < nchunks + D; ++c) {
-        rc = retire((int)(c % D));
-        if (rc) goto done;
-    }
-done:
-    if (sh) cudaStreamSynchronize(sh);
-    if (sc) cudaStreamSynchronize(sc);
-    if (sd) cudaStreamSynchronize(sd);
-    for (int i = 0; i < D; ++i) {
-        if (dbuf[i]) cudaFree(dbuf[i]);
-        if (hbuf[i]) cudaFreeHost(hbuf[i]);
-        if (ev_made) {
-            cudaEventDestroy(e0[i]);
-            cudaEventDestroy(e1[i]);
-            cudaEventDestroy(e2[i]);
-            cudaEventDestroy(e3[i]);
+        if (!hout) hout = c->hbuf[i];
+#define CKL(call)                                                                                       \
+        if ((ce = (call)) != cudaSuccess) {                                                             \
+            rc = bfft_set_error(FFT_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(ce));            \
+            break;                                                                                      \
         }
+        CKL(cudaEventRecord(c->e0[i], c->sh));
+        CKL(cudaMemcpyAsync(c->dbuf[i], hin, (size_t)(cnt * rb), cudaMemcpyHostToDevice, c->sh));
+        CKL(cudaEventRecord(c->e1[i], c->sh));
+        CKL(cudaStreamWaitEvent(c->sc, c->e1[i], 0));
+        rc = fft_exec_range(c->plan, c->dbuf[i], c->dbuf[i], cnt, c->sc);
+        if (rc) break;
+        CKL(cudaEventRecord(c->e2[i], c->sc));
+        CKL(cudaStreamWaitEvent(c->sd, c->e2[i], 0));
+        CKL(cudaMemcpyAsync(hout, c->dbuf[i], (size_t)(cnt * rb), cudaMemcpyDeviceToHost, c->sd));
+        CKL(cudaEventRecord(c->e3[i], c->sd));
+#undef CKL
+        slot_first[i] = f;
+        slot_count[i] = cnt;
+        st->records += cnt;
+        st->chunks += 1;
+        st->bytes_in += cnt * rb;
     }
-    if (sh) cudaStreamDestroy(sh);
-    if (sc) cudaStreamDestroy(sc);
-    if (sd) cudaStreamDestroy(sd);
-    fft_plan_destroy(plan);
+    for (int64_t k = nchunks; rc == FFT_OK && k < nchunks + D; ++k) rc = retire((int)(k % D));
+    if (rc) {
+        cudaStreamSynchronize(c->sh);
+        cudaStreamSynchronize(c->sc);
+        cudaStreamSynchronize(c->sd);
+    }
+    release_ctx(c, rc != FFT_OK);
     return rc;
 }
 
@@ -413,6 +502,22 @@ extern "C" int fft_file_ex(const char* in_path, const char* out_path, int64_t n,
     agg.s.ngpu = ngpu;
     if (stats) *stats = agg.s;
     return rc;
+}
+
+extern "C" int fft_stream_release(void) {
+    std::lock_guard<std::mutex> g(g_ctx_mu);
+    int freed = 0;
+    for (size_t i = 0; i < g_ctx.size();) {
+        if (!g_ctx[i]->busy) {
+            g_ctx[i]->release();
+            delete g_ctx[i];
+            g_ctx.erase(g_ctx.begin() + (long)i);
+            ++freed;
+        } else {
+            ++i;
+        }
+    }
+    return freed;
 }
 
 extern "C" int fft_file(const char* in_path, const char* out_path, int64_t record_len, int ngpu) {
