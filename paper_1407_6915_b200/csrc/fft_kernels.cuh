@@ -67,7 +67,7 @@ __host__ __device__ constexpr int tw_entries_rt(int L, int P) {
     return tot;
 }
 // Lengths with a constant table: P = 16 for L in [32, 2048], P = 32 for L in [64, 512].
-__host__ __device__ constexpr int ctw_max_l(int P) { return P == 16 ? 2048 : 512; }
+__host__ __device__ constexpr int ctw_max_l(int P) { return P == 16 ? 2048 : 1024; }
 constexpr int CTW_MIN_L = 32;
 // offset of the (L, P) table in c_tw; pairs ordered by P in {16, 32}, then L
 __host__ __device__ constexpr int const_tw_base(int L, int P) {

@@ -268,11 +268,12 @@ __device__ __forceinline__ void red_relaxed_gpu(int* p, int v) {
     asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int N1, int N2, int COLS, int ROWS, int NSTAGE>
+template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP = 16>
 struct Pipe2Cfg {
     static constexpr int N = N1 * N2;
-    static constexpr int NTC = COLS * Sched<N1>::T;            // compute threads
-    static_assert(ROWS * Sched<N2>::T == NTC, "A and B tasks use the same compute warps");
+    static constexpr int NTC = COLS * Sched<N1, PP>::T;        // compute threads
+    static_assert(ROWS * Sched<N2, PP>::T == NTC, "A and B tasks use the same compute warps");
+    static_assert(Sched<N1, PP>::P == PP && Sched<N2, PP>::P == PP, "N1, N2 >= PP");
     static_assert(NTC % 32 == 0, "whole compute warps");
     static constexpr int NT = NTC + 64;                          // + producer warp + release warp
     static constexpr int TA = N2 / COLS, TB = N1 / ROWS;
@@ -281,7 +282,7 @@ struct Pipe2Cfg {
     static constexpr int TILE = TILE_A > TILE_B ? TILE_A : TILE_B;
     static constexpr int BOXR = N1 < 256 ? N1 : 256;             // TMA box rows
     static constexpr size_t SMEM = sizeof(float2) * (size_t)TILE * NSTAGE + 64 * NSTAGE + 128;
-    static constexpr int MINB_RAW = 65536 / (NT * 64);
+    static constexpr int MINB_RAW = 65536 / (NT * (PP == 16 ? 64 : 96));
     static constexpr int MINB = MINB_RAW < 1 ? 1 : (MINB_RAW > 8 ? 8 : MINB_RAW);
 };
 
@@ -291,14 +292,16 @@ struct PipeTask {
     int tile;       // column tile (A) or row tile (B)
 };
 
-template <int N1, int N2, int COLS, int ROWS, bool INV, int NSTAGE>
-__global__ void __launch_bounds__(Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE>::NT, Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE>::MINB)
+template <int N1, int N2, int COLS, int ROWS, bool INV, int NSTAGE, int PP = 16>
+__global__ void __launch_bounds__(Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>::NT,
+                                  Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>::MINB)
 k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, float2* __restrict__ ring,
         int64_t nrec, int* __restrict__ ctr, int S, int LAG, float scale, const float2* __restrict__ w_hi,
         const float2* __restrict__ w_lo, int w_lb) {
-    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE>;
+    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>;
+    constexpr int LPP = ilog2(PP);
     constexpr int N = CF::N, TA = CF::TA, TB = CF::TB, NTC = CF::NTC, TILE = CF::TILE, RSTRIDE = CF::RSTRIDE;
-    constexpr int TA1 = Sched<N1>::T, TB2 = Sched<N2>::T;
+    constexpr int TA1 = Sched<N1, PP>::T, TB2 = Sched<N2, PP>::T;
     extern __shared__ __align__(128) float2 sm[];
     PipeTask* info = reinterpret_cast<PipeTask*>(sm + (size_t)TILE * NSTAGE);
     uint64_t* bars = reinterpret_cast<uint64_t*>(info + NSTAGE);   // full | empty | done
@@ -418,8 +421,8 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
     } else {
         // ============================================== compute warps
         const TwoLevel W{w_hi, w_lo, w_lb, (uint32_t)(N - 1)};
-        const ConstTw<N1> tabA{};
-        const ConstTw<N2> tabB{};
+        const ConstTw<N1, PP> tabA{};
+        const ConstTw<N2, PP> tabB{};
         const NamedBarrier bar{1, NTC};
         for (uint32_t k = 0;; ++k) {
             const uint32_t s = k % NSTAGE, u = k / NSTAGE;
@@ -431,33 +434,33 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
             float2* stage = sm + (size_t)s * TILE;
             const int64_t r = d.rec;
             const int slot = (int)(r % S);
-            float2 v[16];
+            float2 v[PP];
             if (d.kind == 0) {
                 // ---------------- A: columns n2 of record r, FFT over n1, twiddle, -> ring
                 const int col = tid % COLS, t = tid / COLS;
                 const int n2 = d.tile * COLS + col;
-                float2 f[4], w0;
+                float2 f[LPP], w0;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) f[i] = W((uint32_t)n2 * (uint32_t)(TA1 << i));
+                for (int i = 0; i < LPP; ++i) f[i] = W((uint32_t)n2 * (uint32_t)(TA1 << i));
                 w0 = W((uint32_t)n2 * (uint32_t)t);
 #pragma unroll
-                for (int q = 0; q < 16; ++q) {
+                for (int q = 0; q < PP; ++q) {
                     const float2 x = stage[(t + q * TA1) * COLS + col];
                     v[q] = INV ? conjf2(x) : x;
                 }
-                fft_engine<N1>(v, t, stage, [&](int e) { return ColLayout<COLS>::at(e, col); }, tabA, bar);
-                float2 w[16];
+                fft_engine<N1, PP>(v, t, stage, [&](int e) { return ColLayout<COLS>::at(e, col); }, tabA, bar);
+                float2 w[PP];
                 w[0] = w0;
                 v[0] = cmul(v[0], w0);
 #pragma unroll
-                for (int q = 1; q < 16; ++q) {
-                    const int lb = (q & 1) ? 0 : (q & 2) ? 1 : (q & 4) ? 2 : 3;
+                for (int q = 1; q < PP; ++q) {
+                    const int lb = (q & 1) ? 0 : (q & 2) ? 1 : (q & 4) ? 2 : (q & 8) ? 3 : 4;
                     w[q] = cmul(w[q & (q - 1)], f[lb]);
                     v[q] = cmul(v[q], w[q]);
                 }
                 float2* dst = ring + (int64_t)slot * N + n2 + (int64_t)t * N2;
 #pragma unroll
-                for (int q = 0; q < 16; ++q) dst[(int64_t)q * TA1 * N2] = v[q];
+                for (int q = 0; q < PP; ++q) dst[(int64_t)q * TA1 * N2] = v[q];
             } else {
                 // ---------------- B: rows k1 of record r, FFT over n2, -> X[k1 + N1 k2]
                 const int col = tid % ROWS, t = tid / ROWS;
@@ -467,11 +470,11 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                     for (int i = tid; i < ROWS * N2 * 8 / 128; i += NTC) l2_discard128(rows + 128 * i);
                 }
 #pragma unroll
-                for (int q = 0; q < 16; ++q) v[q] = stage[col * RSTRIDE + t + q * TB2];
-                fft_engine<N2>(v, t, stage, [&](int e) { return ColLayout<ROWS>::at(e, col); }, tabB, bar);
+                for (int q = 0; q < PP; ++q) v[q] = stage[col * RSTRIDE + t + q * TB2];
+                fft_engine<N2, PP>(v, t, stage, [&](int e) { return ColLayout<ROWS>::at(e, col); }, tabB, bar);
                 float2* dst = out + r * N + k0 + col + (int64_t)t * N1;
 #pragma unroll
-                for (int q = 0; q < 16; ++q)
+                for (int q = 0; q < PP; ++q)
                     st_stream(dst + (int64_t)q * TB2 * N1, INV ? scale_conj(v[q], scale) : v[q]);
             }
             __syncwarp();

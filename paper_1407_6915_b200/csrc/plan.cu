@@ -246,13 +246,13 @@ static ClusterChoice pick_cluster(int log2n, int want_c, bool inv) {
 }
 
 struct PipeChoice {
-    int n1 = 0, n2 = 0, cols = 0, rows = 0, impl = 1, boxr = 0, stages = 0;
+    int n1 = 0, n2 = 0, cols = 0, rows = 0, impl = 1, boxr = 0, stages = 0, pp = 16;
     KernelSet k;
 };
 using Pipe2Fn = void (*)(const CUtensorMap, float2*, float2*, int64_t, int*, int, int, float, const float2*,
                          const float2*, int);
-template <int N1, int N2, int COLS, int ROWS, int NSTAGE> static PipeChoice pipe2_kernel(bool inv) {
-    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE>;
+template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP = 16> static PipeChoice pipe2_kernel(bool inv) {
+    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>;
     PipeChoice ch;
     ch.n1 = N1;
     ch.n2 = N2;
@@ -261,8 +261,9 @@ template <int N1, int N2, int COLS, int ROWS, int NSTAGE> static PipeChoice pipe
     ch.impl = 2;
     ch.stages = NSTAGE;
     ch.boxr = CF::BOXR;
-    ch.k.fn = inv ? (const void*)&k_pipe2<N1, N2, COLS, ROWS, true, NSTAGE>
-                  : (const void*)&k_pipe2<N1, N2, COLS, ROWS, false, NSTAGE>;
+    ch.k.fn = inv ? (const void*)&k_pipe2<N1, N2, COLS, ROWS, true, NSTAGE, PP>
+                  : (const void*)&k_pipe2<N1, N2, COLS, ROWS, false, NSTAGE, PP>;
+    ch.pp = PP;
     ch.k.threads = CF::NT;
     ch.k.smem = CF::SMEM;
     return ch;
@@ -296,15 +297,21 @@ static PipeChoice pick_pipe(int log2n, bool inv) {
             case 13: return pipe2_pick<128, 64, 16, 32>(inv);
             case 14: return pipe2_pick<128, 128, 16, 16>(inv);
             case 15: return pipe2_pick<256, 128, 16, 32>(inv);
-            case 16: return pipe2_pick<256, 256, 16, 16>(inv);
+            case 16:
+                if (getenv("BLOCKFFT_PIPE_TINY")) return pipe2_pick<256, 256, 8, 8>(inv);
+                return pipe2_pick<256, 256, 16, 16>(inv);
             case 17:
                 if (getenv("BLOCKFFT_PIPE_WIDE")) return pipe2_pick<512, 256, 16, 32>(inv);
                 return pipe2_pick<512, 256, 8, 16>(inv);
             case 18:
                 if (getenv("BLOCKFFT_PIPE_WIDE")) return pipe2_pick<512, 512, 16, 16>(inv);
                 return pipe2_pick<512, 512, 8, 8>(inv);
-            case 19: return pipe2_pick<1024, 512, 8, 16>(inv);
-            case 20: return pipe2_pick<1024, 1024, 8, 8>(inv);
+            case 19:
+                if (getenv("BLOCKFFT_PIPE_P16")) return pipe2_pick<1024, 512, 8, 16>(inv);
+                return pipe2_kernel<1024, 512, 8, 16, 2, 32>(inv);
+            case 20:
+                if (getenv("BLOCKFFT_PIPE_P16")) return pipe2_pick<1024, 1024, 8, 8>(inv);
+                return pipe2_kernel<1024, 1024, 8, 8, 2, 32>(inv);
             default: return PipeChoice{};
         }
     }
