@@ -316,6 +316,7 @@ static PipeChoice pick_pipe(int log2n, bool inv) {
         }
     }
     switch (log2n) {
+        case 13: return pipe_kernel<128, 64, 16, 32>(inv);
         case 14: return pipe_kernel<128, 128, 16, 16>(inv);
         case 15: return pipe_kernel<256, 128, 32, 64>(inv);
         case 16:

@@ -148,3 +148,30 @@ def test_file_errors(tmp_path):
         bf.fft_file(str(good), str(out), 1024, 99)
     assert ei.value.code == 5
     assert not out.exists() and not os.path.exists(str(out) + ".tmp")
+
+
+def test_stream_cache_and_release(tmp_path):
+    # repeated streamed calls reuse cached per-GPU resources; release frees them
+    n = 4096
+    s = torch.from_numpy(synth.random_records(6, n, 0, 40)).pin_memory()
+    out1 = torch.empty_like(s).pin_memory()
+    out2 = torch.empty_like(s).pin_memory()
+    bf.exec_host(s, n, bf.FFT_FORWARD, 0, out=out1, chunk_bytes=8 * n * 16)
+    bf.exec_host(s, n, bf.FFT_FORWARD, 0, out=out2, chunk_bytes=8 * n * 16)
+    assert torch.equal(out1, out2)
+    assert bf.stream_release() >= 1
+    bf.exec_host(s, n, bf.FFT_FORWARD, 0, out=out2, chunk_bytes=8 * n * 16)
+    assert torch.equal(out1, out2)
+
+
+@pytest.mark.parametrize("n", [1 << 13, 1 << 16])
+def test_file_inverse_roundtrip_pipelined(tmp_path, n):
+    # the default (pipelined four-step) variant through the file pipeline, both directions
+    s = synth.random_samples(12, 0, 19 * n)
+    a, b, c = tmp_path / "a", tmp_path / "b", tmp_path / "c"
+    write_file(a, s)
+    bf.fft_file(str(a), str(b), n, 1, direction=bf.FFT_FORWARD, chunk_bytes=8 * n * 6)
+    ref = oracle.file_transform(a.read_bytes(), n)
+    assert np.all(oracle.rel_l2(read_c64(b, n), ref) <= oracle.tolerance(n))
+    bf.fft_file(str(b), str(c), n, 1, direction=bf.FFT_INVERSE, chunk_bytes=8 * n * 5)
+    assert np.all(oracle.rel_l2(read_c64(c, n), s.reshape(-1, n)) <= 2 * oracle.tolerance(n))

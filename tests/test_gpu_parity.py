@@ -214,3 +214,30 @@ def test_report_quality_band():
     print("\nquality (max rel L2) per case:", {f"{k}": f"{v:.2e}" for k, v in sorted(_quality.items())})
     if worst:
         print("above quality band:", worst)
+
+
+@pytest.mark.parametrize("impl,n", [(0, 1 << 15), (0, 1 << 16), (1, 1 << 14), (1, 1 << 16), (2, 1 << 14),
+                                    (2, 1 << 16)])
+def test_cluster_implementations(monkeypatch, impl, n):
+    # every cluster implementation (TMA-staged, single-buffer, pipelined) stays exact
+    monkeypatch.setenv("BLOCKFFT_CLUSTER_IMPL", str(impl))
+    x = synth.random_records(41 + impl, n, 0, 7)
+    check(x, bf.FFT_FORWARD, bf.VARIANT_CLUSTER)
+    check(x, bf.FFT_INVERSE, bf.VARIANT_CLUSTER)
+
+
+@pytest.mark.parametrize("impl,n", [(1, 1 << 13), (1, 1 << 16), (1, 1 << 20), (2, 1 << 13), (2, 1 << 17),
+                                    (2, 1 << 20)])
+def test_pipe_implementations(monkeypatch, impl, n):
+    monkeypatch.setenv("BLOCKFFT_PIPE_IMPL", str(impl))
+    b = 5 if n >= (1 << 20) else 33
+    x = synth.random_records(53 + impl, n, 0, b)
+    check(x, bf.FFT_FORWARD, bf.VARIANT_PIPE)
+    check(x, bf.FFT_INVERSE, bf.VARIANT_PIPE)
+
+
+def test_auto_variant_choice():
+    # AUTO picks the single-pass kernel up to 2^12 and the pipelined four-step above
+    for n, want in ((2, "single"), (4096, "single"), (8192, "pipe"), (1 << 16, "pipe"), (1 << 22, "pipe")):
+        with bf.Plan(n, 2) as p:
+            assert p.info()["variant_name"] == want, n
