@@ -149,7 +149,7 @@ typedef struct fft_stream_opts {
                              or env BLOCKFFT_CHUNK_BYTES                         */
     int depth;            /* pipeline buffers per stage (>= 2); 0 = default 3  */
     int variant;          /* enum fft_variant for the per-chunk plan (0=auto)  */
-    int io_threads;       /* host I/O threads per GPU for file pread/pwrite; 0 = 4 */
+    int io_threads;       /* host threads splitting each chunk's pread/pwrite; 0 = 8 */
 } fft_stream_opts;
 
 typedef struct fft_stream_stats {

@@ -88,19 +88,56 @@ int pwrite_full(int fd, const void* buf, int64_t len, int64_t off) {
     return 0;
 }
 
+// A chunk's pread/pwrite split over `nt` threads (>= 8 MiB each): one thread
+// moves only a few GB/s through the page cache, the host's memory system far
+// more, and the file path is host-I/O bound (I/O dominates).
+template <class F>
+int parallel_io(int64_t len, int nt, F&& piece) {
+    const int64_t min_piece = 8ll << 20;
+    nt = (int)std::max<int64_t>(1, std::min<int64_t>(nt, len / min_piece));
+    if (nt == 1) return piece(0, len);
+    std::vector<std::thread> th;
+    std::vector<int> rc(nt, 0);
+    const int64_t step = ((len / nt) + 4095) & ~4095ll;
+    for (int i = 0; i < nt; ++i) {
+        const int64_t a = i * step, b = std::min<int64_t>(len, a + step);
+        if (a >= b) break;
+        th.emplace_back([&, i, a, b]() { rc[i] = piece(a, b - a); });
+    }
+    for (auto& t : th) t.join();
+    for (int r : rc)
+        if (r) return r;
+    return 0;
+}
+
 // File source: record r is at byte r*rb; bytes past EOF read as zero
 // (the final record is zero-padded, reading c6).
 struct FileSource : Source {
     int fd;
     int64_t size, rb;
     const char* path;
-    FileSource(int f, int64_t s, int64_t recbytes, const char* p) : fd(f), size(s), rb(recbytes), path(p) {}
+    int nt;
+    FileSource(int f, int64_t s, int64_t recbytes, const char* p, int threads)
+        : fd(f), size(s), rb(recbytes), path(p), nt(threads) {}
     int read(int64_t first, int64_t count, void* dst) override {
         const int64_t off = first * rb, len = count * rb;
         const int64_t avail = std::max<int64_t>(0, std::min<int64_t>(len, size - off));
-        int64_t got = 0;
-        if (avail > 0 && (pread_full(fd, dst, avail, off, &got) != 0 || got != avail))
-            return io_err("short read of", path, off, avail, got);
+        if (avail > 0) {
+            int64_t bad_got = 0, bad_off = 0, bad_want = 0;
+            std::mutex m;
+            int r = parallel_io(avail, nt, [&](int64_t a, int64_t n) {
+                int64_t got = 0;
+                if (pread_full(fd, (char*)dst + a, n, off + a, &got) != 0 || got != n) {
+                    std::lock_guard<std::mutex> g(m);
+                    bad_got = got;
+                    bad_off = off + a;
+                    bad_want = n;
+                    return 1;
+                }
+                return 0;
+            });
+            if (r) return io_err("short read of", path, bad_off, bad_want, bad_got);
+        }
         if (avail < len) memset((char*)dst + avail, 0, (size_t)(len - avail));
         return FFT_OK;
     }
@@ -109,11 +146,21 @@ struct FileSink : Sink {
     int fd;
     int64_t rb;
     const char* path;
-    FileSink(int f, int64_t recbytes, const char* p) : fd(f), rb(recbytes), path(p) {}
+    int nt;
+    FileSink(int f, int64_t recbytes, const char* p, int threads) : fd(f), rb(recbytes), path(p), nt(threads) {}
     int write(int64_t first, int64_t count, const void* src) override {
-        if (pwrite_full(fd, src, count * rb, first * rb) != 0)
-            return bfft_set_error(FFT_E_IO, "write of %s at offset %lld failed: %s", path,
-                                  (long long)(first * rb), strerror(errno));
+        const int64_t off = first * rb;
+        int err = 0;
+        int r = parallel_io(count * rb, nt, [&](int64_t a, int64_t n) {
+            if (pwrite_full(fd, (const char*)src + a, n, off + a) != 0) {
+                err = errno;
+                return 1;
+            }
+            return 0;
+        });
+        if (r)
+            return bfft_set_error(FFT_E_IO, "write of %s at offset %lld failed: %s", path, (long long)off,
+                                  strerror(err));
         return FFT_OK;
     }
 };
@@ -172,6 +219,7 @@ struct Opts {
     int64_t chunk_bytes = 256ll << 20;
     int depth = 3;
     int variant = FFT_VARIANT_AUTO;
+    int io_threads = 8;
 };
 
 Opts resolve(const fft_stream_opts* o) {
@@ -181,6 +229,7 @@ Opts resolve(const fft_stream_opts* o) {
         if (o->chunk_bytes > 0) r.chunk_bytes = o->chunk_bytes;
         if (o->depth >= 2) r.depth = o->depth;
         r.variant = o->variant;
+        if (o->io_threads > 0) r.io_threads = o->io_threads;
     }
     return r;
 }
@@ -476,8 +525,8 @@ extern "C" int fft_file_ex(const char* in_path, const char* out_path, int64_t n,
                 int64_t first = 0, count = 0;
                 fft_partition(R, ngpu, g, &first, &count);
                 if (count == 0) return;
-                FileSource src(fd, size, 8 * n, in_path);
-                FileSink dst(ofd, 8 * n, tmp.c_str());
+                FileSource src(fd, size, 8 * n, in_path, o.io_threads);
+                FileSink dst(ofd, 8 * n, tmp.c_str(), o.io_threads);
                 fft_stream_stats st{};
                 rcs[g] = run_pipeline(g, n, dir, first, count, &src, &dst, o, &st);
                 if (rcs[g]) msgs[g] = fft_last_error();
