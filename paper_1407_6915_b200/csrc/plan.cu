@@ -293,19 +293,21 @@ static PipeChoice pick_pipe(int log2n, bool inv) {
     int impl = (log2n >= 13 && log2n <= 20) ? 2 : 1;
     if (const char* e = getenv("BLOCKFFT_PIPE_IMPL")) impl = atoi(e);
     if (impl == 2) {
+        // radix-32 engines (32 points per thread) where measured faster, else radix-16
+        const bool p32 = getenv("BLOCKFFT_PIPE_P32") ? atoi(getenv("BLOCKFFT_PIPE_P32")) != 0 : (log2n >= 15);
         switch (log2n) {
-            case 13: return pipe2_pick<128, 64, 16, 32>(inv);
-            case 14: return pipe2_pick<128, 128, 16, 16>(inv);
-            case 15: return pipe2_pick<256, 128, 16, 32>(inv);
+            case 13: return p32 ? pipe2_kernel<128, 64, 16, 32, 2, 32>(inv) : pipe2_pick<128, 64, 16, 32>(inv);
+            case 14: return p32 ? pipe2_kernel<128, 128, 16, 16, 2, 32>(inv) : pipe2_pick<128, 128, 16, 16>(inv);
+            case 15: return p32 ? pipe2_kernel<256, 128, 16, 32, 2, 32>(inv) : pipe2_pick<256, 128, 16, 32>(inv);
             case 16:
                 if (getenv("BLOCKFFT_PIPE_TINY")) return pipe2_pick<256, 256, 8, 8>(inv);
-                return pipe2_pick<256, 256, 16, 16>(inv);
+                return p32 ? pipe2_kernel<256, 256, 16, 16, 2, 32>(inv) : pipe2_pick<256, 256, 16, 16>(inv);
             case 17:
                 if (getenv("BLOCKFFT_PIPE_WIDE")) return pipe2_pick<512, 256, 16, 32>(inv);
-                return pipe2_pick<512, 256, 8, 16>(inv);
+                return p32 ? pipe2_kernel<512, 256, 8, 16, 2, 32>(inv) : pipe2_pick<512, 256, 8, 16>(inv);
             case 18:
                 if (getenv("BLOCKFFT_PIPE_WIDE")) return pipe2_pick<512, 512, 16, 16>(inv);
-                return pipe2_pick<512, 512, 8, 8>(inv);
+                return p32 ? pipe2_kernel<512, 512, 8, 8, 2, 32>(inv) : pipe2_pick<512, 512, 8, 8>(inv);
             case 19:
                 if (getenv("BLOCKFFT_PIPE_P16")) return pipe2_pick<1024, 512, 8, 16>(inv);
                 return pipe2_kernel<1024, 512, 8, 16, 2, 32>(inv);
