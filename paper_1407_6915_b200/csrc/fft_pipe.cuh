@@ -371,11 +371,13 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                     mbar_arrive(fb);
                 } else {
                     const int slot = (int)(d.rec % S), gen = (int)(d.rec / S);
+#ifndef BFFT_PIPE_NODEPS  // (experiments only: tools/exp measures the kernel without its waits)
                     if (d.kind == 0) {
                         if (gen > 0) wait_geq(doneB + slot, gen * TB);   // ring slot free (WAR)
                     } else {
                         wait_geq(doneA + slot, (gen + 1) * TA);          // column FFTs published
                     }
+#endif
                     info[s] = d;
                     mbar_expect_tx(fb, (uint32_t)((d.kind == 0 ? CF::TILE_A : ROWS * N2) * sizeof(float2)));
                 }
@@ -410,7 +412,9 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 mbar_wait(done0 + 8 * s, u & 1);
                 P2_T(rt1)
                 mbar_arrive(empty0 + 8 * s);   // stage reusable (compute warps are past it)
+#ifndef BFFT_PIPE_NODEPS
                 fence_acq_rel_gpu();            // their stores, observed through done[s], become visible
+#endif
                 const int slot = (int)(d.rec % S);
                 red_relaxed_gpu((d.kind == 0 ? doneA : doneB) + slot, 1);
                 P2_T(rt2)
