@@ -155,22 +155,22 @@ __device__ __forceinline__ void twiddle_row16(uint32_t m0, uint32_t dm, uint32_t
 // ======================================================================
 // E1: single-pass, B records per CTA, one record = T threads x P points.
 // ======================================================================
-template <int L, int B>
+template <int L, int B, int PP = 16>
 struct RowsMinBlocks {  // CTAs per SM the register budget is sized for
-    static constexpr int THREADS = B * Sched<L>::T;
-    static constexpr int V = THREADS <= 256 ? 3 : 1;
+    static constexpr int THREADS = B * Sched<L, PP>::T;
+    static constexpr int V = PP == 32 ? (THREADS <= 256 ? 2 : 1) : (THREADS <= 256 ? 3 : 1);
 };
 
-template <int L, int B, bool INV>
-__global__ void __launch_bounds__(B * Sched<L>::T, RowsMinBlocks<L, B>::V)
+template <int L, int B, bool INV, int PP = 16>
+__global__ void __launch_bounds__(B * Sched<L, PP>::T, RowsMinBlocks<L, B, PP>::V)
 k_rows(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
        const float2* __restrict__ tw, float scale) {
-    using S = Sched<L>;
+    using S = Sched<L, PP>;
     constexpr int P = S::P, T = S::T;
     extern __shared__ float2 sm[];
     const int tid = threadIdx.x;
     const int b = tid / T, t = tid - (tid / T) * T;
-    const TableTw<L> tab{tw};
+    const TableTw<L, PP> tab{tw};
     auto addr = [&](int e) { return RowLayout::at(b * L + e); };
     for (int64_t g = blockIdx.x; g * B < nrec; g += gridDim.x) {
         const int64_t r = g * B + b;
@@ -182,7 +182,7 @@ k_rows(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
             float2 x = ok ? ld_stream(src + s * T) : make_float2(0.f, 0.f);
             v[s] = INV ? conjf2(x) : x;
         }
-        fft_engine<L>(v, t, sm, addr, tab);
+        fft_engine<L, PP>(v, t, sm, addr, tab);
         if (ok) {
             float2* dst = out + r * (int64_t)L + t;
 #pragma unroll

@@ -68,11 +68,11 @@ using Cluster2Fn = void (*)(const float2*, float2*, int64_t, float);
 using PipeFn = void (*)(const float2*, float2*, float2*, int64_t, int*, int, int, float, const float2*,
                         const float2*, int);
 
-template <int L> struct RowGeom {
-    static constexpr int T = Sched<L>::T;
+template <int L, int PP = 16> struct RowGeom {
+    static constexpr int T = Sched<L, PP>::T;
     static constexpr int B = T >= 256 ? 1 : 256 / T;  // records per CTA
     static constexpr int THREADS = B * T;
-    static constexpr size_t SMEM = Sched<L>::NPASS > 1 ? sizeof(float2) * RowLayout::size(B * L) : 0;
+    static constexpr size_t SMEM = Sched<L, PP>::NPASS > 1 ? sizeof(float2) * RowLayout::size(B * L) : 0;
 };
 template <int L> struct FsGeom {
     static constexpr int COLS = L >= 2048 ? 8 : 16;   // tile width (columns or rows)
@@ -85,14 +85,17 @@ struct KernelSet {
     int threads = 0;
     size_t smem = 0;
     int cols = 0;
+    int pp = 16;
 };
 
-template <int L> static KernelSet row_kernel(bool inv) {
+template <int L, int PP = 16> static KernelSet row_kernel(bool inv) {
+    using G = RowGeom<L, PP>;
     KernelSet k;
-    k.fn = inv ? (const void*)&k_rows<L, RowGeom<L>::B, true> : (const void*)&k_rows<L, RowGeom<L>::B, false>;
-    k.threads = RowGeom<L>::THREADS;
-    k.smem = RowGeom<L>::SMEM;
-    k.cols = RowGeom<L>::B;
+    k.fn = inv ? (const void*)&k_rows<L, G::B, true, PP> : (const void*)&k_rows<L, G::B, false, PP>;
+    k.threads = G::THREADS;
+    k.smem = G::SMEM;
+    k.cols = G::B;
+    k.pp = PP;
     return k;
 }
 template <int L> static KernelSet fs_col_kernel(int n2, bool inv) {
@@ -125,8 +128,12 @@ static KernelSet pick_row(int log2l, bool inv) {
         BFFT_L_CASES(M)
 #undef M
         case 12: return row_kernel<4096>(inv);
-        case 13: return row_kernel<8192>(inv);
-        case 14: return row_kernel<16384>(inv);
+        case 13:
+            if (getenv("BLOCKFFT_ROWS_P16")) return row_kernel<8192>(inv);
+            return row_kernel<8192, 32>(inv);
+        case 14:
+            if (getenv("BLOCKFFT_ROWS_P16")) return row_kernel<16384>(inv);
+            return row_kernel<16384, 32>(inv);
         default: return KernelSet{};
     }
 }
@@ -450,7 +457,7 @@ static int default_variant(int log2n) {
         if ((v >= 1 && v <= 3) || v == FFT_VARIANT_PIPE) return v;
     }
     // fastest measured per size (profiles/r01_variants_*.txt)
-    if (log2n <= 12) return FFT_VARIANT_SINGLE;
+    if (log2n <= 13) return FFT_VARIANT_SINGLE;
     return FFT_VARIANT_PIPE;
 }
 
@@ -492,7 +499,7 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         p->ka = pick_row(p->log2n, inv);
         p->n1 = (int)n;
         p->n2 = 1;
-        stockham_table((int)n, ta);
+        stockham_table((int)n, ta, p->ka.pp);
     } else if (variant == FFT_VARIANT_CLUSTER) {
         int want = 0;
         if (const char* e = getenv("BLOCKFFT_CLUSTER_SIZE")) want = atoi(e);

@@ -238,6 +238,7 @@ def test_pipe_implementations(monkeypatch, impl, n):
 
 def test_auto_variant_choice():
     # AUTO picks the single-pass kernel up to 2^12 and the pipelined four-step above
-    for n, want in ((2, "single"), (4096, "single"), (8192, "pipe"), (1 << 16, "pipe"), (1 << 22, "pipe")):
+    for n, want in ((2, "single"), (4096, "single"), (8192, "single"), (1 << 14, "pipe"), (1 << 16, "pipe"),
+                    (1 << 22, "pipe")):
         with bf.Plan(n, 2) as p:
             assert p.info()["variant_name"] == want, n

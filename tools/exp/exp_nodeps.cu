@@ -9,8 +9,11 @@
 using namespace bfft;
 extern "C" float exp_run(const void* in, void* out, void* ring, int* ctr, long long nrec, int S, int LAG,
                          const void* hi, const void* lo, int lb) {
-    auto fn = k_pipe2<256, 256, 16, 16, false, 2, 32>;
-    using CF = Pipe2Cfg<256, 256, 16, 16, 2, 32>;
+#ifndef NST
+#define NST 2
+#endif
+    auto fn = k_pipe2<256, 256, 16, 16, false, NST, 32>;
+    using CF = Pipe2Cfg<256, 256, 16, 16, NST, 32>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, CF::NT, CF::SMEM);

@@ -7,11 +7,11 @@ x = torch.randn((b, n), dtype=torch.complex64, device="cuda"); y = torch.empty_l
 lb = 8
 hi = torch.tensor([complex(math.cos(-2*math.pi*(a<<lb)/n), math.sin(-2*math.pi*(a<<lb)/n)) for a in range(n >> lb)], dtype=torch.complex64, device="cuda")
 lo = torch.tensor([complex(math.cos(-2*math.pi*k/n), math.sin(-2*math.pi*k/n)) for k in range(1 << lb)], dtype=torch.complex64, device="cuda")
-for name in ("libnodeps_on.so", "libnodeps_off.so"):
+for name in ("libnodeps_on.so", "libnodeps_on3.so", "libnodeps_off3.so"):
     lib = ctypes.CDLL(os.path.join(ROOT, "tools", "exp", name))
     lib.exp_run.argtypes = [vp, vp, vp, vp, ctypes.c_longlong, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int]
     lib.exp_run.restype = ctypes.c_float
-    for S, LAG in ((149, 64), (121, 60)):
+    for S, LAG in ((149, 64), (200, 80)):
         ring = torch.empty((S, n), dtype=torch.complex64, device="cuda")
         ctr = torch.zeros(1 + 2 * S, dtype=torch.int32, device="cuda")
         ms = lib.exp_run(x.data_ptr(), y.data_ptr(), ring.data_ptr(), ctr.data_ptr(), b, S, LAG, hi.data_ptr(), lo.data_ptr(), lb)
