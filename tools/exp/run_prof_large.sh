@@ -1,0 +1,13 @@
+#!/bin/bash
+# ncu --set full captures of the pipelined four-step at 2^20 (k_pipe2) and 2^22 (k_pipe) + DRAM pattern probe
+cd "$(dirname "$0")/../.."
+mkdir -p gpurun_out
+O=gpurun_out/pl
+timeout 300 python tools/exp/run_dram2.py > ${O}_dram2.txt 2>&1
+for n in 1048576 4194304; do
+  b=$(( (1<<30) / (8*n) ))
+  timeout 300 python tools/ncu_target.py --n $n --batch $b --reps 2 > ${O}_t$n.txt 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pipe -s 1 -c 1 \
+    -o ${O}_$n -f python tools/ncu_target.py --n $n --batch $b --reps 2 > ${O}_ncu$n.log 2>&1
+done
+echo done
