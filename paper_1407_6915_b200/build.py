@@ -38,16 +38,32 @@ def _run(cmd):
     subprocess.check_call(cmd)
 
 
+def _includes(path, seen=None):
+    """Local headers a source includes (recursively, #include "...")."""
+    seen = set() if seen is None else seen
+    d = os.path.dirname(path)
+    with open(path) as f:
+        for line in f:
+            line = line.strip()
+            if line.startswith('#include "'):
+                h = os.path.normpath(os.path.join(d, line.split('"')[1]))
+                if os.path.exists(h) and h not in seen:
+                    seen.add(h)
+                    _includes(h, seen)
+    return sorted(seen)
+
+
 def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(INC, "blockfft.h"))
-    objs = []
-    for src, kind in (("plan.cu", "cu"), ("stream.cpp", "cpp")):
+    objs, cmds = [], []
+    # translation units compile concurrently (each holds its own kernel instantiations)
+    for src, kind in (("plan.cu", "cu"), ("kern_pipe3.cu", "cu"), ("stream.cpp", "cpp")):
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         objs.append(o)
-        if force or _newer(o, [s] + headers):
+        if force or _newer(o, [s] + _includes(s)):
             if kind == "cu":
                 cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                        "-I", INC, "-c", s, "-o", o]
@@ -56,7 +72,14 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
             else:
                 cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-I", INC,
                        "-I", os.path.join(CUDA, "include"), "-c", s, "-o", o]
-            _run(cmd)
+            cmds.append(cmd)
+    procs = []
+    for cmd in cmds:
+        print("+", " ".join(cmd), file=sys.stderr)
+        procs.append((cmd, subprocess.Popen(cmd)))
+    failed = [cmd for cmd, pr in procs if pr.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, failed[0])
     if force or _newer(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lcudart", "-lpthread"])
         os.replace(LIB + ".tmp", LIB)

@@ -276,7 +276,7 @@ k_fs_rows(const float2* __restrict__ y, float2* __restrict__ out, int64_t nrec, 
 // ======================================================================
 // Identity kernel: out = in, bit-exact, 16-byte vectors.
 // ======================================================================
-__global__ void k_copy(const float4* __restrict__ in, float4* __restrict__ out, int64_t n16) {
+static __global__ void k_copy(const float4* __restrict__ in, float4* __restrict__ out, int64_t n16) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16;
          i += (int64_t)gridDim.x * blockDim.x)
         __stcs(out + i, __ldcs(in + i));

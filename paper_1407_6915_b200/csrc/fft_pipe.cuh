@@ -38,6 +38,17 @@ __device__ __forceinline__ void wait_geq(const int* p, int target) {
         ns = ns < 256 ? 2 * ns : ns;
     }
 }
+// wait until *p >= target (acquire); returns the value seen
+__device__ __forceinline__ int wait_geq_v(const int* p, int target) {
+    int v = ld_acquire_gpu(p);
+    int ns = 32;
+    while (v < target) {
+        __nanosleep(ns);
+        ns = ns < 256 ? 2 * ns : ns;
+        v = ld_acquire_gpu(p);
+    }
+    return v;
+}
 __device__ __forceinline__ float2 ld_l2(const float2* p) { return __ldcg(p); }
 // Drop a dead 128-byte line of the ring from L2 without writing it back: once
 // a B-task holds its rows in shared memory the intermediate is dead, and
@@ -90,7 +101,7 @@ struct PipeCfg {
 // Optional phase timing (experiments only: tools/exp/exp_pipe.cu defines
 // BFFT_PIPE_PROF; the product library never does).
 #ifdef BFFT_PIPE_PROF
-__device__ unsigned long long g_pipe_prof[32];
+static __device__ unsigned long long g_pipe_prof[32];
 #define P2_T(v) unsigned long long v = clock64();
 #define P2_ACC(slot, a, b) atomicAdd(&g_pipe_prof[slot], (b) - (a));
 #else

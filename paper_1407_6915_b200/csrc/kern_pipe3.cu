@@ -1,0 +1,63 @@
+// kern_pipe3.cu — instantiations of k_pipe3 (fft_pipe3.cuh) and their picker,
+// compiled as their own translation unit.
+#include <cstdlib>
+
+#include "fft_pipe3.cuh"
+#include "plan_internal.h"
+
+using namespace bfft;
+
+template <int N1, int N2, int COLS, int ROWS, int NS, int G, int CB>
+static PipeChoice pipe3_kernel(bool inv) {
+    using CF = Pipe3Cfg<N1, N2, COLS, ROWS, NS, G, 32>;
+    PipeChoice ch;
+    ch.n1 = N1;
+    ch.n2 = N2;
+    ch.cols = COLS;
+    ch.rows = ROWS;
+    ch.impl = 3;
+    ch.stages = NS + G + CB;   // tasks a CTA holds besides its next claim (stages, groups, claim batch)
+    ch.boxr = CF::BOXR;
+    ch.k.fn = inv ? (const void*)&k_pipe3<N1, N2, COLS, ROWS, true, NS, G, 32, CB>
+                  : (const void*)&k_pipe3<N1, N2, COLS, ROWS, false, NS, G, 32, CB>;
+    ch.pp = 32;
+    ch.k.threads = CF::NT;
+    ch.k.smem = CF::SMEM;
+    return ch;
+}
+
+// (stages, groups, claim batch) per size; env BLOCKFFT_PIPE3_CFG selects the alternatives
+// measured in profiles/ (32 KiB tiles: (4,3,4) / (3,4,4) / (1,2,2) x2 CTAs / (1,2,4) x2 CTAs;
+// 64 KiB tiles: (1,2,1) / (1,2,2))
+template <int N1, int N2, int COLS, int ROWS>
+static PipeChoice pipe3_pick(bool inv) {
+    int c = 0;
+    if (const char* e = getenv("BLOCKFFT_PIPE3_CFG")) c = atoi(e);
+    constexpr size_t tile = sizeof(float2) * (size_t)Pipe3Cfg<N1, N2, COLS, ROWS, 1, 1, 32>::TILE;
+    if constexpr (tile <= 36 * 1024) {
+        if (c == 1) return pipe3_kernel<N1, N2, COLS, ROWS, 3, 4, 4>(inv);
+        if (c == 2) return pipe3_kernel<N1, N2, COLS, ROWS, 1, 2, 2>(inv);   // two CTAs per SM
+        if (c == 3) return pipe3_kernel<N1, N2, COLS, ROWS, 1, 2, 4>(inv);
+        return pipe3_kernel<N1, N2, COLS, ROWS, 4, 3, 4>(inv);
+    } else {
+        if (c == 1) return pipe3_kernel<N1, N2, COLS, ROWS, 1, 2, 2>(inv);
+        return pipe3_kernel<N1, N2, COLS, ROWS, 1, 2, 1>(inv);
+    }
+}
+
+PipeChoice pick_pipe3(int log2n, bool inv) {
+    switch (log2n) {
+        case 15: return pipe3_pick<256, 128, 16, 32>(inv);
+        case 16: return pipe3_pick<256, 256, 16, 16>(inv);
+        case 17: return pipe3_pick<512, 256, 8, 16>(inv);
+        case 18: return pipe3_pick<512, 512, 8, 8>(inv);
+        case 19: return pipe3_pick<1024, 512, 8, 16>(inv);
+        case 20: return pipe3_pick<1024, 1024, 8, 8>(inv);
+        default: return PipeChoice{};
+    }
+}
+
+int pipe3_upload_const(const float2* host, size_t count) {
+    if (count != (size_t)CTW_TOTAL) return 1;
+    return cudaMemcpyToSymbol(c_tw, host, count * sizeof(float2)) == cudaSuccess ? 0 : 1;
+}

@@ -24,6 +24,7 @@
 #include "fft_cluster.cuh"
 #include "fft_pipe.cuh"
 #include "fft_kernels.cuh"
+#include "plan_internal.h"
 
 using namespace bfft;
 
@@ -80,13 +81,6 @@ template <int L> struct FsGeom {
     static constexpr size_t SMEM = sizeof(float2) * COLS * L;
 };
 
-struct KernelSet {
-    const void* fn = nullptr;
-    int threads = 0;
-    size_t smem = 0;
-    int cols = 0;
-    int pp = 16;
-};
 
 template <int L, int PP = 16> static KernelSet row_kernel(bool inv) {
     using G = RowGeom<L, PP>;
@@ -252,10 +246,6 @@ static ClusterChoice pick_cluster(int log2n, int want_c, bool inv) {
     }
 }
 
-struct PipeChoice {
-    int n1 = 0, n2 = 0, cols = 0, rows = 0, impl = 1, boxr = 0, stages = 0, pp = 16;
-    KernelSet k;
-};
 using Pipe2Fn = void (*)(const CUtensorMap, float2*, float2*, int64_t, int*, int, int, float, const float2*,
                          const float2*, int);
 template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP = 16> static PipeChoice pipe2_kernel(bool inv) {
@@ -274,6 +264,9 @@ template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP = 16> static Pi
     ch.k.threads = CF::NT;
     ch.k.smem = CF::SMEM;
     return ch;
+}
+template <int N1, int N2, int COLS, int ROWS> static PipeChoice pipe2_p32(bool inv) {
+    return pipe2_kernel<N1, N2, COLS, ROWS, 2, 32>(inv);
 }
 template <int N1, int N2, int COLS, int ROWS> static PipeChoice pipe2_pick(bool inv) {
     int ns = 2;
@@ -294,27 +287,33 @@ template <int N1, int N2, int COLS, int ROWS> static PipeChoice pipe_kernel(bool
 }
 // Pipelined four-step splits (N1 >= N2; A-tile COLS columns, B-tile ROWS rows).
 static PipeChoice pick_pipe(int log2n, bool inv) {
-    // fastest measured per size (profiles/r01_variants_*): warp-specialised
-    // k_pipe2 for 2^15 and 2^18..2^20, k_pipe otherwise (k_pipe2 also needs
-    // NTC + 64 <= 1024 threads, so not 2^21..2^22)
-    int impl = (log2n >= 13 && log2n <= 20) ? 2 : 1;
+    // fastest measured per size (profiles/r01_variants_*, r01_pipe3_*): k_pipe3
+    // (compute groups, early stage release) for 2^19 and 2^20, warp-specialised
+    // k_pipe2 for 2^13..2^18, k_pipe for 2^21..2^22 (k_pipe2 also needs
+    // NTC + 64 <= 1024 threads)
+    int impl = (log2n >= 19 && log2n <= 20) ? 3 : (log2n >= 13 && log2n <= 20) ? 2 : 1;
     if (const char* e = getenv("BLOCKFFT_PIPE_IMPL")) impl = atoi(e);
+    if (impl == 3) {
+        PipeChoice ch = pick_pipe3(log2n, inv);
+        if (ch.k.fn) return ch;
+        impl = (log2n >= 13 && log2n <= 20) ? 2 : 1;
+    }
     if (impl == 2) {
         // radix-32 engines (32 points per thread) where measured faster, else radix-16
         const bool p32 = getenv("BLOCKFFT_PIPE_P32") ? atoi(getenv("BLOCKFFT_PIPE_P32")) != 0 : (log2n >= 15);
         switch (log2n) {
             case 13: return p32 ? pipe2_kernel<128, 64, 16, 32, 2, 32>(inv) : pipe2_pick<128, 64, 16, 32>(inv);
             case 14: return p32 ? pipe2_kernel<128, 128, 16, 16, 2, 32>(inv) : pipe2_pick<128, 128, 16, 16>(inv);
-            case 15: return p32 ? pipe2_kernel<256, 128, 16, 32, 2, 32>(inv) : pipe2_pick<256, 128, 16, 32>(inv);
+            case 15: return p32 ? pipe2_p32<256, 128, 16, 32>(inv) : pipe2_pick<256, 128, 16, 32>(inv);
             case 16:
                 if (getenv("BLOCKFFT_PIPE_TINY")) return pipe2_pick<256, 256, 8, 8>(inv);
-                return p32 ? pipe2_kernel<256, 256, 16, 16, 2, 32>(inv) : pipe2_pick<256, 256, 16, 16>(inv);
+                return p32 ? pipe2_p32<256, 256, 16, 16>(inv) : pipe2_pick<256, 256, 16, 16>(inv);
             case 17:
                 if (getenv("BLOCKFFT_PIPE_WIDE")) return pipe2_pick<512, 256, 16, 32>(inv);
-                return p32 ? pipe2_kernel<512, 256, 8, 16, 2, 32>(inv) : pipe2_pick<512, 256, 8, 16>(inv);
+                return p32 ? pipe2_p32<512, 256, 8, 16>(inv) : pipe2_pick<512, 256, 8, 16>(inv);
             case 18:
                 if (getenv("BLOCKFFT_PIPE_WIDE")) return pipe2_pick<512, 512, 16, 16>(inv);
-                return p32 ? pipe2_kernel<512, 512, 8, 8, 2, 32>(inv) : pipe2_pick<512, 512, 8, 8>(inv);
+                return p32 ? pipe2_p32<512, 512, 8, 8>(inv) : pipe2_pick<512, 512, 8, 8>(inv);
             case 19:
                 if (getenv("BLOCKFFT_PIPE_P16")) return pipe2_pick<1024, 512, 8, 16>(inv);
                 return pipe2_kernel<1024, 512, 8, 16, 2, 32>(inv);
@@ -417,6 +416,7 @@ static int upload_const_twiddles(int device) {
         }
     if ((int)all.size() != CTW_TOTAL) return bfft_set_error(FFT_E_CUDA, "constant twiddle size mismatch");
     CUDA_TRY(cudaMemcpyToSymbol(c_tw, all.data(), all.size() * sizeof(float2)));
+    if (pipe3_upload_const(all.data(), all.size()) != 0) return bfft_set_error(FFT_E_CUDA, "constant twiddle upload failed");
     done[device] = true;
     return FFT_OK;
 }
@@ -606,7 +606,7 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         // dependencies; measured best on B200 (profiles/r01_pipe_lag_sweep.txt):
         // LAG ~ 1.5x and S - LAG ~ 2x the in-flight rounds.  The ring is capped
         // at 96 MiB so it stays resident in the 126 MB L2.
-        const int stages = ch.impl == 2 ? ch.stages : 0;
+        const int stages = ch.impl >= 2 ? ch.stages : 0;   // k_pipe3: stages + groups
         const int64_t inflight = (int64_t)resident * (stages + 1);
         const int64_t rounds = (inflight + per_round - 1) / per_round;
         p->pipe_LAG = (int)(3 * rounds / 2 + 1);
@@ -741,7 +741,7 @@ static int launch(const fft_plan* p, const float2* in, float2* out, int64_t coun
         case FFT_VARIANT_PIPE: {
             CUDA_TRY(cudaMemsetAsync(p->d_ctr, 0, sizeof(int) * (1 + 2 * p->pipe_S), st));
             const int grid = p->occ_a * p->sms;
-            if (p->pipe_impl == 2) {
+            if (p->pipe_impl >= 2) {
                 CUtensorMap tm;
                 int rc = make_record_tmap(&tm, in, count, p->n1, p->n2, p->ka.cols, p->pipe_boxr);
                 if (rc) return rc;

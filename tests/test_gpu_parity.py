@@ -236,6 +236,32 @@ def test_pipe_implementations(monkeypatch, impl, n):
     check(x, bf.FFT_INVERSE, bf.VARIANT_PIPE)
 
 
+@pytest.mark.parametrize("cfg,n", [(0, 1 << 15), (1, 1 << 16), (2, 1 << 16), (3, 1 << 17), (2, 1 << 18),
+                                   (0, 1 << 19), (1, 1 << 20), (0, 1 << 20)])
+def test_pipe3_configurations(monkeypatch, cfg, n):
+    # k_pipe3 (compute groups with early stage release): every (stages, groups,
+    # claim batch) configuration, both directions
+    monkeypatch.setenv("BLOCKFFT_PIPE_IMPL", "3")
+    monkeypatch.setenv("BLOCKFFT_PIPE3_CFG", str(cfg))
+    b = 5 if n >= (1 << 19) else 33
+    x = synth.random_records(71 + cfg, n, 0, b)
+    check(x, bf.FFT_FORWARD, bf.VARIANT_PIPE)
+    check(x, bf.FFT_INVERSE, bf.VARIANT_PIPE)
+
+
+@pytest.mark.parametrize("cfg", [0, 2])
+def test_pipe3_ring_reuse_many_records(monkeypatch, cfg):
+    # several full turns of the ring: WAR waits, claim batches across record boundaries
+    monkeypatch.setenv("BLOCKFFT_PIPE_IMPL", "3")
+    monkeypatch.setenv("BLOCKFFT_PIPE3_CFG", str(cfg))
+    n = 1 << 15
+    with bf.Plan(n, 1, bf.FFT_FORWARD, bf.VARIANT_PIPE) as p:
+        s = p.info()["scratch_bytes"] // (8 * n)
+    b = 3 * s + 5
+    x = synth.random_records(77 + cfg, n, 0, b)
+    check(x, bf.FFT_FORWARD, bf.VARIANT_PIPE)
+
+
 def test_auto_variant_choice():
     # AUTO picks the single-pass kernel up to 2^12 and the pipelined four-step above
     for n, want in ((2, "single"), (4096, "single"), (8192, "single"), (1 << 14, "pipe"), (1 << 16, "pipe"),
