@@ -73,9 +73,16 @@ __device__ __forceinline__ int ld_acquire_cta_s(const int* p) {
 __device__ __forceinline__ void st_release_cta_s(int* p, int v) {
     asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
 }
+// L2 prefetch of one TMA box (no shared memory, no barrier)
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* tmap, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmap)),
+                 "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
 __device__ __forceinline__ int ld_volatile_s(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 
-template <int N1, int N2, int COLS, int ROWS, bool INV, int NS, int G, int PP = 32, int CB = 4>
+template <int N1, int N2, int COLS, int ROWS, bool INV, int NS, int G, int PP = 32, int CB = 4, bool PF = false>
 __global__ void __launch_bounds__(Pipe3Cfg<N1, N2, COLS, ROWS, NS, G, PP>::NT, Pipe3Cfg<N1, N2, COLS, ROWS, NS, G, PP>::MINB)
 k_pipe3(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, float2* __restrict__ ring,
         int64_t nrec, int* __restrict__ ctr, int S, int LAG, float scale, const float2* __restrict__ w_hi,
@@ -170,6 +177,11 @@ k_pipe3(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
             const uint32_t s = k % NS, u = k / NS;
             const uint32_t fb = full0 + 8 * s;
             if (lane == 0) {
+                if (PF && d.kind == 0) {
+                    // pull the A-tile from HBM into L2 while the stage is still busy
+#pragma unroll 1
+                    for (int r0 = 0; r0 < N1; r0 += CF::BOXR) tma_prefetch_3d(&tmap_in, d.tile * COLS, r0, (int)d.rec);
+                }
                 if (u > 0) mbar_wait(empty0 + 8 * s, (u - 1) & 1);   // task k - NS read out of the stage
                 const int slot = (int)(d.rec % S), gen = (int)(d.rec / S);
                 const int* dp = nullptr;

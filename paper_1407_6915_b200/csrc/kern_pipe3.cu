@@ -7,7 +7,7 @@
 
 using namespace bfft;
 
-template <int N1, int N2, int COLS, int ROWS, int NS, int G, int CB>
+template <int N1, int N2, int COLS, int ROWS, int NS, int G, int CB, bool PF = false>
 static PipeChoice pipe3_kernel(bool inv) {
     using CF = Pipe3Cfg<N1, N2, COLS, ROWS, NS, G, 32>;
     PipeChoice ch;
@@ -18,8 +18,8 @@ static PipeChoice pipe3_kernel(bool inv) {
     ch.impl = 3;
     ch.stages = NS + G + CB;   // tasks a CTA holds besides its next claim (stages, groups, claim batch)
     ch.boxr = CF::BOXR;
-    ch.k.fn = inv ? (const void*)&k_pipe3<N1, N2, COLS, ROWS, true, NS, G, 32, CB>
-                  : (const void*)&k_pipe3<N1, N2, COLS, ROWS, false, NS, G, 32, CB>;
+    ch.k.fn = inv ? (const void*)&k_pipe3<N1, N2, COLS, ROWS, true, NS, G, 32, CB, PF>
+                  : (const void*)&k_pipe3<N1, N2, COLS, ROWS, false, NS, G, 32, CB, PF>;
     ch.pp = 32;
     ch.k.threads = CF::NT;
     ch.k.smem = CF::SMEM;
@@ -28,7 +28,7 @@ static PipeChoice pipe3_kernel(bool inv) {
 
 // (stages, groups, claim batch) per size; env BLOCKFFT_PIPE3_CFG selects the alternatives
 // measured in profiles/ (32 KiB tiles: (4,3,4) / (3,4,4) / (1,2,2) x2 CTAs / (1,2,4) x2 CTAs;
-// 64 KiB tiles: (1,2,1) / (1,2,2))
+// 64 KiB tiles: (1,2,1) / (1,2,2) / (1,2,1)+L2 prefetch / (1,2,2)+L2 prefetch; 4 = (1,2,2)+prefetch, 32 KiB)
 template <int N1, int N2, int COLS, int ROWS>
 static PipeChoice pipe3_pick(bool inv) {
     int c = 0;
@@ -38,9 +38,12 @@ static PipeChoice pipe3_pick(bool inv) {
         if (c == 1) return pipe3_kernel<N1, N2, COLS, ROWS, 3, 4, 4>(inv);
         if (c == 2) return pipe3_kernel<N1, N2, COLS, ROWS, 1, 2, 2>(inv);   // two CTAs per SM
         if (c == 3) return pipe3_kernel<N1, N2, COLS, ROWS, 1, 2, 4>(inv);
+        if (c == 4) return pipe3_kernel<N1, N2, COLS, ROWS, 1, 2, 2, true>(inv);
         return pipe3_kernel<N1, N2, COLS, ROWS, 4, 3, 4>(inv);
     } else {
         if (c == 1) return pipe3_kernel<N1, N2, COLS, ROWS, 1, 2, 2>(inv);
+        if (c == 2) return pipe3_kernel<N1, N2, COLS, ROWS, 1, 2, 1, true>(inv);
+        if (c == 3) return pipe3_kernel<N1, N2, COLS, ROWS, 1, 2, 2, true>(inv);
         return pipe3_kernel<N1, N2, COLS, ROWS, 1, 2, 1>(inv);
     }
 }

@@ -3,7 +3,7 @@
 # (stages, groups) configurations against k_pipe2
 cd "$(dirname "$0")/../.."
 BLOCKFFT_PIPE_IMPL=3 timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "pipe" 2>&1 | tail -3
-for c in ${CFGS:-0 1 2 3}; do
+for c in ${CFGS:-0 1 2 3 4}; do
   echo "== k_pipe3 cfg=$c"
   BLOCKFFT_PIPE_IMPL=3 BLOCKFFT_PIPE3_CFG=$c timeout 240 python tools/time_variants.py --min ${MINL:-15} --max ${MAXL:-20} --variants 5 2>&1 | grep -v "^$"
 done
