@@ -118,6 +118,11 @@ def ncu_traffic(kernel_substr, n, batch):
     for k in d.get("kernels", []):
         if kernel_substr in k.get("name", "") and k.get("n") == n and k.get("batch") == batch:
             return k.get("dram_bytes_per_launch"), k.get("source")
+    # same kernel and N captured at another batch: per-record DRAM bytes scale with the batch
+    for k in d.get("kernels", []):
+        if kernel_substr in k.get("name", "") and k.get("n") == n and k.get("batch"):
+            per = k["dram_bytes_per_launch"] / k["batch"]
+            return per * batch, f"{k.get('source')} (captured at batch {k['batch']}, scaled per record)"
     return None, None
 
 
