@@ -290,7 +290,8 @@ struct Pipe2Cfg {
     static constexpr int TA = N2 / COLS, TB = N1 / ROWS;
     static constexpr int RSTRIDE = N2 + 2;                       // padded B-tile row (16-B multiple)
     static constexpr int TILE_A = COLS * N1, TILE_B = ROWS * RSTRIDE;
-    static constexpr int TILE = TILE_A > TILE_B ? TILE_A : TILE_B;
+    // stage stride rounded to 128 bytes: TMA writes shared memory at 128-byte aligned addresses
+    static constexpr int TILE = ((TILE_A > TILE_B ? TILE_A : TILE_B) + 15) / 16 * 16;
     static constexpr int BOXR = N1 < 256 ? N1 : 256;             // TMA box rows
     static constexpr size_t SMEM = sizeof(float2) * (size_t)TILE * NSTAGE + 64 * NSTAGE + 128;
     static constexpr int MINB_RAW = 65536 / (NT * (PP == 16 ? 64 : 96));

@@ -287,11 +287,10 @@ template <int N1, int N2, int COLS, int ROWS> static PipeChoice pipe_kernel(bool
 }
 // Pipelined four-step splits (N1 >= N2; A-tile COLS columns, B-tile ROWS rows).
 static PipeChoice pick_pipe(int log2n, bool inv) {
-    // fastest measured per size (profiles/r01_variants_*, r01_pipe3_*): k_pipe3
-    // (compute groups, early stage release) for 2^19 and 2^20, warp-specialised
-    // k_pipe2 for 2^13..2^18, k_pipe for 2^21..2^22 (k_pipe2 also needs
-    // NTC + 64 <= 1024 threads)
-    int impl = (log2n >= 19 && log2n <= 20) ? 3 : (log2n >= 13 && log2n <= 20) ? 2 : 1;
+    // fastest measured per size (profiles/r01_variants_*, r01_pipe3_*, r01_pipe2_large.txt):
+    // k_pipe3 (compute groups, early stage release) for 2^19 and 2^20, warp-specialised
+    // k_pipe2 for 2^13..2^18 and 2^21..2^22 (radix-16, 64 KiB tiles); k_pipe on request
+    int impl = (log2n >= 19 && log2n <= 20) ? 3 : (log2n >= 13 && log2n <= 22) ? 2 : 1;
     if (const char* e = getenv("BLOCKFFT_PIPE_IMPL")) impl = atoi(e);
     if (impl == 3) {
         PipeChoice ch = pick_pipe3(log2n, inv);
@@ -320,6 +319,9 @@ static PipeChoice pick_pipe(int log2n, bool inv) {
             case 20:
                 if (getenv("BLOCKFFT_PIPE_P16")) return pipe2_pick<1024, 1024, 8, 8>(inv);
                 return pipe2_kernel<1024, 1024, 8, 8, 2, 32>(inv);
+            // radix-16 engines (the constant twiddles hold L = 2048 for P = 16 only), 64 KiB tiles
+            case 21: return pipe2_kernel<2048, 1024, 4, 8, 2, 16>(inv);
+            case 22: return pipe2_kernel<2048, 2048, 4, 4, 2, 16>(inv);
             default: return PipeChoice{};
         }
     }

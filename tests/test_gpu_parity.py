@@ -226,8 +226,8 @@ def test_cluster_implementations(monkeypatch, impl, n):
     check(x, bf.FFT_INVERSE, bf.VARIANT_CLUSTER)
 
 
-@pytest.mark.parametrize("impl,n", [(1, 1 << 13), (1, 1 << 16), (1, 1 << 20), (2, 1 << 13), (2, 1 << 17),
-                                    (2, 1 << 20)])
+@pytest.mark.parametrize("impl,n", [(1, 1 << 13), (1, 1 << 16), (1, 1 << 20), (1, 1 << 21), (1, 1 << 22),
+                                    (2, 1 << 13), (2, 1 << 17), (2, 1 << 20)])
 def test_pipe_implementations(monkeypatch, impl, n):
     monkeypatch.setenv("BLOCKFFT_PIPE_IMPL", str(impl))
     b = 5 if n >= (1 << 20) else 33
