@@ -59,7 +59,8 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     headers.append(os.path.join(INC, "blockfft.h"))
     objs, cmds = [], []
     # translation units compile concurrently (each holds its own kernel instantiations)
-    for src, kind in (("plan.cu", "cu"), ("kern_pipe3.cu", "cu"), ("stream.cpp", "cpp")):
+    for src, kind in (("plan.cu", "cu"), ("kern_rows.cu", "cu"), ("kern_cluster.cu", "cu"), ("kern_pipe.cu", "cu"),
+                      ("kern_pipe3.cu", "cu"), ("stream.cpp", "cpp")):
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         objs.append(o)

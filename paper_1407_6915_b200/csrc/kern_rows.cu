@@ -1,0 +1,93 @@
+// kern_rows.cu — single-pass row kernels (k_rows) and the two-kernel four-step (k_fs_cols, k_fs_rows): instantiations and pickers, compiled as its own translation unit
+// (kernel instantiations dominate build time; plan.cu only dispatches).
+#include <cstdlib>
+
+#include "fft_kernels.cuh"
+#include "plan_internal.h"
+
+using namespace bfft;
+
+template <int L, int PP = 16> struct RowGeom {
+    static constexpr int T = Sched<L, PP>::T;
+    static constexpr int B = T >= 256 ? 1 : 256 / T;  // records per CTA
+    static constexpr int THREADS = B * T;
+    static constexpr size_t SMEM = Sched<L, PP>::NPASS > 1 ? sizeof(float2) * RowLayout::size(B * L) : 0;
+};
+template <int L> struct FsGeom {
+    static constexpr int COLS = L >= 2048 ? 8 : 16;   // tile width (columns or rows)
+    static constexpr int THREADS = COLS * Sched<L>::T;
+    static constexpr size_t SMEM = sizeof(float2) * COLS * L;
+};
+
+
+template <int L, int PP = 16> static KernelSet row_kernel(bool inv) {
+    using G = RowGeom<L, PP>;
+    KernelSet k;
+    k.fn = inv ? (const void*)&k_rows<L, G::B, true, PP> : (const void*)&k_rows<L, G::B, false, PP>;
+    k.threads = G::THREADS;
+    k.smem = G::SMEM;
+    k.cols = G::B;
+    k.pp = PP;
+    return k;
+}
+template <int L> static KernelSet fs_col_kernel(int n2, bool inv) {
+    constexpr int C = FsGeom<L>::COLS;
+    KernelSet k;
+    k.fn = inv ? (const void*)&k_fs_cols<L, C, true> : (const void*)&k_fs_cols<L, C, false>;
+    k.threads = FsGeom<L>::THREADS;
+    k.smem = Sched<L>::NPASS > 1 ? FsGeom<L>::SMEM : 0;
+    k.cols = C;
+    (void)n2;
+    return k;
+}
+template <int L> static KernelSet fs_row_kernel(bool inv) {
+    constexpr int C = FsGeom<L>::COLS;
+    KernelSet k;
+    k.fn = inv ? (const void*)&k_fs_rows<L, C, true> : (const void*)&k_fs_rows<L, C, false>;
+    k.threads = FsGeom<L>::THREADS;
+    k.smem = FsGeom<L>::SMEM;  // the transposing tile load always uses shared memory
+    k.cols = C;
+    return k;
+}
+
+#define BFFT_L_CASES(M) \
+    M(1, 2) M(2, 4) M(3, 8) M(4, 16) M(5, 32) M(6, 64) M(7, 128) M(8, 256) M(9, 512) M(10, 1024) \
+    M(11, 2048)
+
+KernelSet pick_row(int log2l, bool inv) {
+    switch (log2l) {
+#define M(k, L) case k: return row_kernel<L>(inv);
+        BFFT_L_CASES(M)
+#undef M
+        case 12: return row_kernel<4096>(inv);
+        case 13:
+            if (getenv("BLOCKFFT_ROWS_P16")) return row_kernel<8192>(inv);
+            return row_kernel<8192, 32>(inv);
+        case 14:
+            if (getenv("BLOCKFFT_ROWS_P16")) return row_kernel<16384>(inv);
+            return row_kernel<16384, 32>(inv);
+        default: return KernelSet{};
+    }
+}
+KernelSet pick_fs_col(int log2l, int n2, bool inv) {
+    switch (log2l) {
+#define M(k, L) case k: return fs_col_kernel<L>(n2, inv);
+        BFFT_L_CASES(M)
+#undef M
+        default: return KernelSet{};
+    }
+}
+KernelSet pick_fs_row(int log2l, bool inv) {
+    switch (log2l) {
+#define M(k, L) case k: return fs_row_kernel<L>(inv);
+        BFFT_L_CASES(M)
+#undef M
+        default: return KernelSet{};
+    }
+}
+
+
+int rows_upload_const(const float2* host, size_t count) {
+    if (count != (size_t)CTW_TOTAL) return 1;
+    return cudaMemcpyToSymbol(c_tw, host, count * sizeof(float2)) == cudaSuccess ? 0 : 1;
+}

@@ -21,8 +21,6 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
-#include "fft_cluster.cuh"
-#include "fft_pipe.cuh"
 #include "fft_kernels.cuh"
 #include "plan_internal.h"
 
@@ -59,288 +57,7 @@ extern "C" int fft_version(void) { return BLOCKFFT_VERSION; }
             return bfft_set_error(FFT_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
     } while (0)
 
-// ------------------------------------------------------------ kernel tables
-using RowFn = void (*)(const float2*, float2*, int64_t, const float2*, float);
-using ColFn = void (*)(const float2*, float2*, int64_t, int, const float2*);
-using RowTFn = void (*)(const float2*, float2*, int64_t, int, const float2*, float);
-using ClusterFn = void (*)(const CUtensorMap, float2*, int64_t, const float2*, const float2*, float);
-using Cluster1Fn = void (*)(const float2*, float2*, int64_t, const float2*, const float2*, float);
-using Cluster2Fn = void (*)(const float2*, float2*, int64_t, float);
-using PipeFn = void (*)(const float2*, float2*, float2*, int64_t, int*, int, int, float, const float2*,
-                        const float2*, int);
-
-template <int L, int PP = 16> struct RowGeom {
-    static constexpr int T = Sched<L, PP>::T;
-    static constexpr int B = T >= 256 ? 1 : 256 / T;  // records per CTA
-    static constexpr int THREADS = B * T;
-    static constexpr size_t SMEM = Sched<L, PP>::NPASS > 1 ? sizeof(float2) * RowLayout::size(B * L) : 0;
-};
-template <int L> struct FsGeom {
-    static constexpr int COLS = L >= 2048 ? 8 : 16;   // tile width (columns or rows)
-    static constexpr int THREADS = COLS * Sched<L>::T;
-    static constexpr size_t SMEM = sizeof(float2) * COLS * L;
-};
-
-
-template <int L, int PP = 16> static KernelSet row_kernel(bool inv) {
-    using G = RowGeom<L, PP>;
-    KernelSet k;
-    k.fn = inv ? (const void*)&k_rows<L, G::B, true, PP> : (const void*)&k_rows<L, G::B, false, PP>;
-    k.threads = G::THREADS;
-    k.smem = G::SMEM;
-    k.cols = G::B;
-    k.pp = PP;
-    return k;
-}
-template <int L> static KernelSet fs_col_kernel(int n2, bool inv) {
-    constexpr int C = FsGeom<L>::COLS;
-    KernelSet k;
-    k.fn = inv ? (const void*)&k_fs_cols<L, C, true> : (const void*)&k_fs_cols<L, C, false>;
-    k.threads = FsGeom<L>::THREADS;
-    k.smem = Sched<L>::NPASS > 1 ? FsGeom<L>::SMEM : 0;
-    k.cols = C;
-    (void)n2;
-    return k;
-}
-template <int L> static KernelSet fs_row_kernel(bool inv) {
-    constexpr int C = FsGeom<L>::COLS;
-    KernelSet k;
-    k.fn = inv ? (const void*)&k_fs_rows<L, C, true> : (const void*)&k_fs_rows<L, C, false>;
-    k.threads = FsGeom<L>::THREADS;
-    k.smem = FsGeom<L>::SMEM;  // the transposing tile load always uses shared memory
-    k.cols = C;
-    return k;
-}
-
-#define BFFT_L_CASES(M) \
-    M(1, 2) M(2, 4) M(3, 8) M(4, 16) M(5, 32) M(6, 64) M(7, 128) M(8, 256) M(9, 512) M(10, 1024) \
-    M(11, 2048)
-
-static KernelSet pick_row(int log2l, bool inv) {
-    switch (log2l) {
-#define M(k, L) case k: return row_kernel<L>(inv);
-        BFFT_L_CASES(M)
-#undef M
-        case 12: return row_kernel<4096>(inv);
-        case 13:
-            if (getenv("BLOCKFFT_ROWS_P16")) return row_kernel<8192>(inv);
-            return row_kernel<8192, 32>(inv);
-        case 14:
-            if (getenv("BLOCKFFT_ROWS_P16")) return row_kernel<16384>(inv);
-            return row_kernel<16384, 32>(inv);
-        default: return KernelSet{};
-    }
-}
-static KernelSet pick_fs_col(int log2l, int n2, bool inv) {
-    switch (log2l) {
-#define M(k, L) case k: return fs_col_kernel<L>(n2, inv);
-        BFFT_L_CASES(M)
-#undef M
-        default: return KernelSet{};
-    }
-}
-static KernelSet pick_fs_row(int log2l, bool inv) {
-    switch (log2l) {
-#define M(k, L) case k: return fs_row_kernel<L>(inv);
-        BFFT_L_CASES(M)
-#undef M
-        default: return KernelSet{};
-    }
-}
-
-struct ClusterChoice {
-    int n1 = 0, n2 = 0, c = 0, pp = 16, impl = 0;
-    KernelSet k;
-};
-static int cluster_xch() {
-    const char* e = getenv("BLOCKFFT_CLUSTER_XCH");
-    return e ? atoi(e) : XCH_STAS;
-}
-template <int N1, int N2, int C> static ClusterChoice cluster_kernel(bool inv) {
-    using CF = ClusterCfg<N1, N2, C>;
-    ClusterChoice ch;
-    ch.n1 = N1;
-    ch.n2 = N2;
-    ch.c = C;
-    if (cluster_xch() == XCH_BULK)
-        ch.k.fn = inv ? (const void*)&k_cluster<N1, N2, C, true, XCH_BULK> : (const void*)&k_cluster<N1, N2, C, false, XCH_BULK>;
-    else
-        ch.k.fn = inv ? (const void*)&k_cluster<N1, N2, C, true, XCH_STAS> : (const void*)&k_cluster<N1, N2, C, false, XCH_STAS>;
-    ch.k.threads = CF::NT;
-    ch.k.smem = CF::SMEM;
-    return ch;
-}
-template <int N1, int N2, int C, int MINB = 0> static ClusterChoice cluster1_kernel(bool inv) {
-    using CF = Cluster1Cfg<N1, N2, C, 32, MINB>;
-    ClusterChoice ch;
-    ch.n1 = N1;
-    ch.n2 = N2;
-    ch.c = C;
-    ch.pp = 32;
-    ch.impl = 1;
-    ch.k.fn = inv ? (const void*)&k_cluster1<N1, N2, C, true, 32, MINB> : (const void*)&k_cluster1<N1, N2, C, false, 32, MINB>;
-    ch.k.threads = CF::NT;
-    ch.k.smem = CF::SMEM;
-    return ch;
-}
-template <int N1, int N2, int C, int PP = 16> static ClusterChoice cluster2_kernel(bool inv) {
-    using CF = Cluster2Cfg<N1, N2, C, PP>;
-    ClusterChoice ch;
-    ch.n1 = N1;
-    ch.n2 = N2;
-    ch.c = C;
-    ch.pp = PP;
-    ch.impl = 2;
-    ch.k.fn = inv ? (const void*)&k_cluster2<N1, N2, C, true, PP> : (const void*)&k_cluster2<N1, N2, C, false, PP>;
-    ch.k.threads = CF::NT;
-    ch.k.smem = CF::SMEM;
-    return ch;
-}
-// Cluster configurations: N = N1*N2 over C CTAs.
-// impl 1 (default): single-buffer k_cluster1; impl 0: TMA-staged k_cluster.
-static ClusterChoice pick_cluster(int log2n, int want_c, bool inv) {
-    // default implementation per size: the fastest measured on B200
-    // (profiles/variants_r01.md): single-buffer k_cluster1 for 2^13..2^15 and
-    // 2^18, TMA-staged k_cluster with st.async exchange and C = 16 for 2^16..2^17.
-    int impl = (log2n <= 15 || log2n >= 18) ? 1 : 0;
-    if (const char* e = getenv("BLOCKFFT_CLUSTER_IMPL")) impl = atoi(e);
-    if (impl == 0 && want_c == 0) want_c = 16;
-    if (impl == 2) {
-        switch (log2n) {
-            case 13: return cluster2_kernel<64, 128, 4>(inv);
-            case 14: return cluster2_kernel<128, 128, 4>(inv);
-            case 15: return cluster2_kernel<128, 256, 8>(inv);
-            case 16:
-                if (want_c == 8) return cluster2_kernel<256, 256, 8>(inv);
-                return cluster2_kernel<256, 256, 16>(inv);
-            case 17: return cluster2_kernel<256, 512, 16>(inv);
-            default: return ClusterChoice{};
-        }
-    }
-    int minb = log2n == 16 ? 4 : 0;
-    if (const char* e = getenv("BLOCKFFT_CLUSTER_MINB")) minb = atoi(e);
-    if (impl == 1) {
-        switch (log2n) {
-            case 13: return minb == 4 ? cluster1_kernel<64, 128, 4, 4>(inv) : cluster1_kernel<64, 128, 4, 6>(inv);
-            case 14: return minb == 4 ? cluster1_kernel<128, 128, 4, 4>(inv) : cluster1_kernel<128, 128, 4, 3>(inv);
-            case 15: return minb == 4 ? cluster1_kernel<128, 256, 8, 4>(inv) : cluster1_kernel<128, 256, 8, 3>(inv);
-            case 16:
-                if (want_c == 16) return minb == 4 ? cluster1_kernel<256, 256, 16, 4>(inv) : cluster1_kernel<256, 256, 16, 3>(inv);
-                return minb == 2 ? cluster1_kernel<256, 256, 8, 2>(inv) : cluster1_kernel<256, 256, 8, 1>(inv);
-            case 17:
-                if (want_c == 8) return cluster1_kernel<256, 512, 8, 1>(inv);
-                return minb == 2 ? cluster1_kernel<256, 512, 16, 2>(inv) : cluster1_kernel<256, 512, 16, 1>(inv);
-            case 18: return cluster1_kernel<512, 512, 16, 1>(inv);
-            default: return ClusterChoice{};
-        }
-    }
-    switch (log2n) {
-        case 13: return cluster_kernel<64, 128, 4>(inv);
-        case 14: return cluster_kernel<128, 128, 4>(inv);
-        case 15: return cluster_kernel<128, 256, 8>(inv);
-        case 16:
-            if (want_c == 16) return cluster_kernel<256, 256, 16>(inv);
-            return cluster_kernel<256, 256, 8>(inv);
-        case 17: return cluster_kernel<256, 512, 16>(inv);
-        default: return ClusterChoice{};
-    }
-}
-
-using Pipe2Fn = void (*)(const CUtensorMap, float2*, float2*, int64_t, int*, int, int, float, const float2*,
-                         const float2*, int);
-template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP = 16> static PipeChoice pipe2_kernel(bool inv) {
-    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>;
-    PipeChoice ch;
-    ch.n1 = N1;
-    ch.n2 = N2;
-    ch.cols = COLS;
-    ch.rows = ROWS;
-    ch.impl = 2;
-    ch.stages = NSTAGE;
-    ch.boxr = CF::BOXR;
-    ch.k.fn = inv ? (const void*)&k_pipe2<N1, N2, COLS, ROWS, true, NSTAGE, PP>
-                  : (const void*)&k_pipe2<N1, N2, COLS, ROWS, false, NSTAGE, PP>;
-    ch.pp = PP;
-    ch.k.threads = CF::NT;
-    ch.k.smem = CF::SMEM;
-    return ch;
-}
-template <int N1, int N2, int COLS, int ROWS> static PipeChoice pipe2_p32(bool inv) {
-    return pipe2_kernel<N1, N2, COLS, ROWS, 2, 32>(inv);
-}
-template <int N1, int N2, int COLS, int ROWS> static PipeChoice pipe2_pick(bool inv) {
-    int ns = 2;
-    if (const char* e = getenv("BLOCKFFT_PIPE_STAGES")) ns = atoi(e);
-    return ns == 3 ? pipe2_kernel<N1, N2, COLS, ROWS, 3>(inv) : pipe2_kernel<N1, N2, COLS, ROWS, 2>(inv);
-}
-template <int N1, int N2, int COLS, int ROWS> static PipeChoice pipe_kernel(bool inv) {
-    using CF = PipeCfg<N1, N2, COLS, ROWS>;
-    PipeChoice ch;
-    ch.n1 = N1;
-    ch.n2 = N2;
-    ch.cols = COLS;
-    ch.rows = ROWS;
-    ch.k.fn = inv ? (const void*)&k_pipe<N1, N2, COLS, ROWS, true> : (const void*)&k_pipe<N1, N2, COLS, ROWS, false>;
-    ch.k.threads = CF::NT;
-    ch.k.smem = CF::SMEM;
-    return ch;
-}
-// Pipelined four-step splits (N1 >= N2; A-tile COLS columns, B-tile ROWS rows).
-static PipeChoice pick_pipe(int log2n, bool inv) {
-    // fastest measured per size (profiles/r01_variants_*, r01_pipe3_*, r01_pipe2_large.txt):
-    // k_pipe3 (compute groups, early stage release) for 2^19 and 2^20, warp-specialised
-    // k_pipe2 for 2^13..2^18 and 2^21..2^22 (radix-16, 64 KiB tiles); k_pipe on request
-    int impl = (log2n >= 19 && log2n <= 20) ? 3 : (log2n >= 13 && log2n <= 22) ? 2 : 1;
-    if (const char* e = getenv("BLOCKFFT_PIPE_IMPL")) impl = atoi(e);
-    if (impl == 3) {
-        PipeChoice ch = pick_pipe3(log2n, inv);
-        if (ch.k.fn) return ch;
-        impl = (log2n >= 13 && log2n <= 20) ? 2 : 1;
-    }
-    if (impl == 2) {
-        // radix-32 engines (32 points per thread) where measured faster, else radix-16
-        const bool p32 = getenv("BLOCKFFT_PIPE_P32") ? atoi(getenv("BLOCKFFT_PIPE_P32")) != 0 : (log2n >= 15);
-        switch (log2n) {
-            case 13: return p32 ? pipe2_kernel<128, 64, 16, 32, 2, 32>(inv) : pipe2_pick<128, 64, 16, 32>(inv);
-            case 14: return p32 ? pipe2_kernel<128, 128, 16, 16, 2, 32>(inv) : pipe2_pick<128, 128, 16, 16>(inv);
-            case 15: return p32 ? pipe2_p32<256, 128, 16, 32>(inv) : pipe2_pick<256, 128, 16, 32>(inv);
-            case 16:
-                if (getenv("BLOCKFFT_PIPE_TINY")) return pipe2_pick<256, 256, 8, 8>(inv);
-                return p32 ? pipe2_p32<256, 256, 16, 16>(inv) : pipe2_pick<256, 256, 16, 16>(inv);
-            case 17:
-                if (getenv("BLOCKFFT_PIPE_WIDE")) return pipe2_pick<512, 256, 16, 32>(inv);
-                return p32 ? pipe2_p32<512, 256, 8, 16>(inv) : pipe2_pick<512, 256, 8, 16>(inv);
-            case 18:
-                if (getenv("BLOCKFFT_PIPE_WIDE")) return pipe2_pick<512, 512, 16, 16>(inv);
-                return p32 ? pipe2_p32<512, 512, 8, 8>(inv) : pipe2_pick<512, 512, 8, 8>(inv);
-            case 19:
-                if (getenv("BLOCKFFT_PIPE_P16")) return pipe2_pick<1024, 512, 8, 16>(inv);
-                return pipe2_kernel<1024, 512, 8, 16, 2, 32>(inv);
-            case 20:
-                if (getenv("BLOCKFFT_PIPE_P16")) return pipe2_pick<1024, 1024, 8, 8>(inv);
-                return pipe2_kernel<1024, 1024, 8, 8, 2, 32>(inv);
-            // radix-16 engines (the constant twiddles hold L = 2048 for P = 16 only), 64 KiB tiles
-            case 21: return pipe2_kernel<2048, 1024, 4, 8, 2, 16>(inv);
-            case 22: return pipe2_kernel<2048, 2048, 4, 4, 2, 16>(inv);
-            default: return PipeChoice{};
-        }
-    }
-    switch (log2n) {
-        case 13: return pipe_kernel<128, 64, 16, 32>(inv);
-        case 14: return pipe_kernel<128, 128, 16, 16>(inv);
-        case 15: return pipe_kernel<256, 128, 32, 64>(inv);
-        case 16:
-            if (getenv("BLOCKFFT_PIPE_WIDE")) return pipe_kernel<256, 256, 32, 32>(inv);
-            return pipe_kernel<256, 256, 16, 16>(inv);
-        case 17: return pipe_kernel<512, 256, 16, 32>(inv);
-        case 18: return pipe_kernel<512, 512, 16, 16>(inv);
-        case 19: return pipe_kernel<1024, 512, 8, 16>(inv);
-        case 20: return pipe_kernel<1024, 1024, 8, 8>(inv);
-        case 21: return pipe_kernel<2048, 1024, 8, 16>(inv);
-        case 22: return pipe_kernel<2048, 2048, 8, 8>(inv);
-        default: return PipeChoice{};
-    }
-}
+// ------------------------------------------------------------ kernel tables: kern_*.cu (plan_internal.h)
 
 // ------------------------------------------------------------ TMA tensor maps
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -418,7 +135,9 @@ static int upload_const_twiddles(int device) {
         }
     if ((int)all.size() != CTW_TOTAL) return bfft_set_error(FFT_E_CUDA, "constant twiddle size mismatch");
     CUDA_TRY(cudaMemcpyToSymbol(c_tw, all.data(), all.size() * sizeof(float2)));
-    if (pipe3_upload_const(all.data(), all.size()) != 0) return bfft_set_error(FFT_E_CUDA, "constant twiddle upload failed");
+    if (pipe3_upload_const(all.data(), all.size()) != 0 || rows_upload_const(all.data(), all.size()) != 0 ||
+        cluster_upload_const(all.data(), all.size()) != 0 || pipe_upload_const(all.data(), all.size()) != 0)
+        return bfft_set_error(FFT_E_CUDA, "constant twiddle upload failed");
     done[device] = true;
     return FFT_OK;
 }

@@ -2,6 +2,8 @@
 // the separately compiled kernel units (kern_*.cu).
 #pragma once
 #include <cstddef>
+#include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 struct KernelSet {
@@ -16,6 +18,37 @@ struct PipeChoice {
     int n1 = 0, n2 = 0, cols = 0, rows = 0, impl = 1, boxr = 0, stages = 0, pp = 16;
     KernelSet k;
 };
+
+struct ClusterChoice {
+    int n1 = 0, n2 = 0, c = 0, pp = 16, impl = 0;
+    KernelSet k;
+};
+
+// kernel signatures, by family (launch casts KernelSet::fn to these)
+using RowFn = void (*)(const float2*, float2*, int64_t, const float2*, float);
+using ColFn = void (*)(const float2*, float2*, int64_t, int, const float2*);
+using RowTFn = void (*)(const float2*, float2*, int64_t, int, const float2*, float);
+using ClusterFn = void (*)(const CUtensorMap, float2*, int64_t, const float2*, const float2*, float);
+using Cluster1Fn = void (*)(const float2*, float2*, int64_t, const float2*, const float2*, float);
+using Cluster2Fn = void (*)(const float2*, float2*, int64_t, float);
+using PipeFn = void (*)(const float2*, float2*, float2*, int64_t, int*, int, int, float, const float2*,
+                        const float2*, int);
+
+using Pipe2Fn = void (*)(const CUtensorMap, float2*, float2*, int64_t, int*, int, int, float, const float2*,
+                         const float2*, int);
+
+// kern_rows.cu: single-pass row kernel for 2^log2l; four-step column / row kernels
+KernelSet pick_row(int log2l, bool inv);
+KernelSet pick_fs_col(int log2l, int n2, bool inv);
+KernelSet pick_fs_row(int log2l, bool inv);
+// kern_cluster.cu: cluster kernel for 2^log2n (want_c = requested cluster size or 0)
+ClusterChoice pick_cluster(int log2n, int want_c, bool inv);
+// kern_pipe.cu: pipelined four-step (k_pipe / k_pipe2, or k_pipe3 through pick_pipe3)
+PipeChoice pick_pipe(int log2n, bool inv);
+// each kernel unit's copy of the constant twiddles (same contents as plan.cu's); 0 on success
+int rows_upload_const(const float2* host, size_t count);
+int cluster_upload_const(const float2* host, size_t count);
+int pipe_upload_const(const float2* host, size_t count);
 
 // kern_pipe3.cu: k_pipe3 (compute groups with early stage release) for 2^log2n
 // (empty choice if that size has no k_pipe3 configuration)
