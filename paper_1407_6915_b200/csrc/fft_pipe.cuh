@@ -464,7 +464,9 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                     const float2 x = stage[(t + q * TA1) * COLS + col];
                     v[q] = INV ? conjf2(x) : x;
                 }
+#ifndef BFFT_PIPE_NOCOMPUTE  // (experiments only: data movement without the FFT)
                 fft_engine<N1, PP>(v, t, stage, [&](int e) { return ColLayout<COLS>::at(e, col); }, tabA, bar);
+#endif
                 float2 w[PP];
                 w[0] = w0;
                 v[0] = cmul(v[0], w0);
@@ -487,7 +489,9 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 }
 #pragma unroll
                 for (int q = 0; q < PP; ++q) v[q] = stage[col * RSTRIDE + t + q * TB2];
+#ifndef BFFT_PIPE_NOCOMPUTE
                 fft_engine<N2, PP>(v, t, stage, [&](int e) { return ColLayout<ROWS>::at(e, col); }, tabB, bar);
+#endif
                 float2* dst = out + r * N + k0 + col + (int64_t)t * N1;
 #pragma unroll
                 for (int q = 0; q < PP; ++q)
