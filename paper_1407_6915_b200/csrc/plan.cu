@@ -87,9 +87,12 @@ static int make_record_tmap(CUtensorMap* m, const void* base, int64_t count, int
     cuuint64_t strides[2] = {(cuuint64_t)n2 * 8, (cuuint64_t)n1 * n2 * 8};
     cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
     cuuint32_t es[3] = {1, 1, 1};
+    // L2 promotion 256 B: a 128-byte column-tile row fetches its neighbour tile's half too
+    // (experiments: BLOCKFFT_TMAP_PROMO = 0 none, 1 64 B, 2 128 B, 3 256 B)
+    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    if (const char* e = getenv("BLOCKFFT_TMAP_PROMO")) promo = (CUtensorMapL2promotion)std::min(3, std::max(0, atoi(e)));
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return bfft_set_error(FFT_E_CUDA, "cuTensorMapEncodeTiled failed: CUresult %d", (int)r);
     return FFT_OK;
 }
