@@ -63,7 +63,9 @@ ClusterChoice pick_cluster(int log2n, int want_c, bool inv) {
     if (impl == 2) {
         switch (log2n) {
             case 13: return cluster2_kernel<64, 128, 4>(inv);
-            case 14: return cluster2_kernel<128, 128, 4>(inv);
+            case 14:
+                if (want_c == 2) return cluster2_kernel<128, 128, 2>(inv);
+                return cluster2_kernel<128, 128, 4>(inv);
             case 15: return cluster2_kernel<128, 256, 8>(inv);
             case 16:
                 if (want_c == 8) return cluster2_kernel<256, 256, 8>(inv);
@@ -77,7 +79,9 @@ ClusterChoice pick_cluster(int log2n, int want_c, bool inv) {
     if (impl == 1) {
         switch (log2n) {
             case 13: return minb == 4 ? cluster1_kernel<64, 128, 4, 4>(inv) : cluster1_kernel<64, 128, 4, 6>(inv);
-            case 14: return minb == 4 ? cluster1_kernel<128, 128, 4, 4>(inv) : cluster1_kernel<128, 128, 4, 3>(inv);
+            case 14:
+                if (want_c == 2) return minb == 3 ? cluster1_kernel<128, 128, 2, 3>(inv) : cluster1_kernel<128, 128, 2, 2>(inv);
+                return minb == 4 ? cluster1_kernel<128, 128, 4, 4>(inv) : cluster1_kernel<128, 128, 4, 3>(inv);
             case 15: return minb == 4 ? cluster1_kernel<128, 256, 8, 4>(inv) : cluster1_kernel<128, 256, 8, 3>(inv);
             case 16:
                 if (want_c == 16) return minb == 4 ? cluster1_kernel<256, 256, 16, 4>(inv) : cluster1_kernel<256, 256, 16, 3>(inv);
@@ -91,7 +95,9 @@ ClusterChoice pick_cluster(int log2n, int want_c, bool inv) {
     }
     switch (log2n) {
         case 13: return cluster_kernel<64, 128, 4>(inv);
-        case 14: return cluster_kernel<128, 128, 4>(inv);
+        case 14:
+            if (want_c == 2) return cluster_kernel<128, 128, 2>(inv);
+            return cluster_kernel<128, 128, 4>(inv);
         case 15: return cluster_kernel<128, 256, 8>(inv);
         case 16:
             if (want_c == 16) return cluster_kernel<256, 256, 16>(inv);
