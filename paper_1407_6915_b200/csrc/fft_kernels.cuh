@@ -161,8 +161,8 @@ struct RowsMinBlocks {  // CTAs per SM the register budget is sized for
     static constexpr int V = PP == 32 ? (THREADS <= 256 ? 2 : 1) : (THREADS <= 256 ? 3 : 1);
 };
 
-template <int L, int B, bool INV, int PP = 16>
-__global__ void __launch_bounds__(B * Sched<L, PP>::T, RowsMinBlocks<L, B, PP>::V)
+template <int L, int B, bool INV, int PP = 16, int MINB = 0>   // MINB > 0 overrides the register budget
+__global__ void __launch_bounds__(B * Sched<L, PP>::T, MINB > 0 ? MINB : RowsMinBlocks<L, B, PP>::V)
 k_rows(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
        const float2* __restrict__ tw, float scale) {
     using S = Sched<L, PP>;

@@ -20,10 +20,10 @@ template <int L> struct FsGeom {
 };
 
 
-template <int L, int PP = 16> static KernelSet row_kernel(bool inv) {
+template <int L, int PP = 16, int MINB = 0> static KernelSet row_kernel(bool inv) {
     using G = RowGeom<L, PP>;
     KernelSet k;
-    k.fn = inv ? (const void*)&k_rows<L, G::B, true, PP> : (const void*)&k_rows<L, G::B, false, PP>;
+    k.fn = inv ? (const void*)&k_rows<L, G::B, true, PP, MINB> : (const void*)&k_rows<L, G::B, false, PP, MINB>;
     k.threads = G::THREADS;
     k.smem = G::SMEM;
     k.cols = G::B;
@@ -62,6 +62,8 @@ KernelSet pick_row(int log2l, bool inv) {
         case 12: return row_kernel<4096>(inv);
         case 13:
             if (getenv("BLOCKFFT_ROWS_P16")) return row_kernel<8192>(inv);
+            if (const char* e = getenv("BLOCKFFT_ROWS_MINB"))   // experiments: 3 CTAs per SM
+                if (atoi(e) == 3) return row_kernel<8192, 32, 3>(inv);
             return row_kernel<8192, 32>(inv);
         case 14:
             if (getenv("BLOCKFFT_ROWS_P16")) return row_kernel<16384>(inv);
