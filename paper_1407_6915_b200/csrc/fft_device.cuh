@@ -252,7 +252,7 @@ struct SwzColLayout {
 // One Stockham pass for a thread holding v[P] = x[t + s*T].  Results are
 // handed to `put(index, value)`; the caller stores them (shared memory, or
 // registers for the last pass).  TW(q, jj) returns W_{Ns*R}^{jj*q}.
-template <int L, int PP, int PASS, class Put, class Tw>
+template <int L, int PP, int PASS, bool DIRECT = false, class Put, class Tw>
 __device__ __forceinline__ void stockham_pass(const float2 (&v)[Sched<L, PP>::P], int t, Put&& put, Tw&& tw) {
     using S = Sched<L, PP>;
     constexpr int P = S::P, T = S::T;
@@ -267,7 +267,7 @@ __device__ __forceinline__ void stockham_pass(const float2 (&v)[Sched<L, PP>::P]
         for (int q = 0; q < R; ++q) a[q] = v[m + q * NB];
         if constexpr (Ns > 1) {
             const int jj = j & (Ns - 1);
-            if constexpr (R <= 8) {
+            if constexpr (R <= 8 || DIRECT) {
 #pragma unroll
                 for (int q = 1; q < R; ++q) a[q] = cmul(a[q], tw(q, jj));
             } else {

@@ -110,6 +110,15 @@ struct NamedBarrier {
     }
 };
 
+// Twiddle source traits: the radix-16/32 passes build their twiddles from
+// log2 R table entries by a multiply tree (fewer loads and live registers);
+// ConstTwDirect reads every product's twiddle from the constant table instead —
+// faster for k_pipe2 radix-32 at 2^16 (57.6 -> 58.6 %), neutral at 2^14/2^15 and slower at
+// 2^17/2^18 and in the other kernels (profiles/r01_twiddle_direct.txt).
+template <int L, int PP = 16> struct ConstTwDirect : ConstTw<L, PP> {};
+template <class Tw> struct tw_direct { static constexpr bool value = false; };
+template <int L, int PP> struct tw_direct<ConstTwDirect<L, PP>> { static constexpr bool value = true; };
+
 template <int L, int PP = 16, class Addr, class Tw, class Bar = CtaBarrier>
 __device__ __forceinline__ void fft_engine(float2 (&v)[Sched<L, PP>::P], int t, float2* sm,
                                            Addr&& addr, const Tw& tw, Bar bar = Bar{}) {
@@ -120,12 +129,12 @@ __device__ __forceinline__ void fft_engine(float2 (&v)[Sched<L, PP>::P], int t, 
         auto twf = [&](int q, int jj) { return tw.template get<PASS>(q, jj); };
         if constexpr (PASS == S::NPASS - 1) {
             float2 o[P];
-            stockham_pass<L, PP, PASS>(v, t, [&](int, int q, int, float2 val) { o[q] = val; }, twf);
+            stockham_pass<L, PP, PASS, tw_direct<Tw>::value>(v, t, [&](int, int q, int, float2 val) { o[q] = val; }, twf);
 #pragma unroll
             for (int q = 0; q < P; ++q) v[q] = o[q];
         } else {
             bar();
-            stockham_pass<L, PP, PASS>(v, t, [&](int idx, int, int, float2 val) { sm[addr(idx)] = val; }, twf);
+            stockham_pass<L, PP, PASS, tw_direct<Tw>::value>(v, t, [&](int idx, int, int, float2 val) { sm[addr(idx)] = val; }, twf);
             bar();
 #pragma unroll
             for (int s = 0; s < P; ++s) v[s] = sm[addr(t + s * T)];

@@ -17,6 +17,8 @@
 // algorithmic minimum) while the transpose traffic stays on chip.
 #pragma once
 
+#include <type_traits>
+
 #include "fft_cluster.cuh"
 #include "fft_kernels.cuh"
 
@@ -304,7 +306,7 @@ struct PipeTask {
     int tile;       // column tile (A) or row tile (B)
 };
 
-template <int N1, int N2, int COLS, int ROWS, bool INV, int NSTAGE, int PP = 16>
+template <int N1, int N2, int COLS, int ROWS, bool INV, int NSTAGE, int PP = 16, bool TWD = false>
 __global__ void __launch_bounds__(Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>::NT,
                                   Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>::MINB)
 k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, float2* __restrict__ ring,
@@ -437,8 +439,9 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
     } else {
         // ============================================== compute warps
         const TwoLevel W{w_hi, w_lo, w_lb, (uint32_t)(N - 1)};
-        const ConstTw<N1, PP> tabA{};
-        const ConstTw<N2, PP> tabB{};
+        // TWD: every Stockham twiddle read from the constant table (no multiply tree)
+        const std::conditional_t<TWD, ConstTwDirect<N1, PP>, ConstTw<N1, PP>> tabA{};
+        const std::conditional_t<TWD, ConstTwDirect<N2, PP>, ConstTw<N2, PP>> tabB{};
         const NamedBarrier bar{1, NTC};
         for (uint32_t k = 0;; ++k) {
             const uint32_t s = k % NSTAGE, u = k / NSTAGE;
