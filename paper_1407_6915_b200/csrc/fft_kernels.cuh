@@ -113,8 +113,9 @@ struct NamedBarrier {
 // Twiddle source traits: the radix-16/32 passes build their twiddles from
 // log2 R table entries by a multiply tree (fewer loads and live registers);
 // ConstTwDirect reads every product's twiddle from the constant table instead —
-// faster for k_pipe2 radix-32 at 2^16 (57.6 -> 58.6 %), neutral at 2^14/2^15 and slower at
-// 2^17/2^18 and in the other kernels (profiles/r01_twiddle_direct.txt).
+// +1 point for k_pipe2 radix-32 at 2^16 alone, nothing on top of the full four-step twiddle
+// table, slower in the other kernels (profiles/r01_twiddle_direct.txt); kept selectable
+// (BLOCKFFT_PIPE_TWD=1).
 template <int L, int PP = 16> struct ConstTwDirect : ConstTw<L, PP> {};
 template <class Tw> struct tw_direct { static constexpr bool value = false; };
 template <int L, int PP> struct tw_direct<ConstTwDirect<L, PP>> { static constexpr bool value = true; };

@@ -306,7 +306,7 @@ struct PipeTask {
     int tile;       // column tile (A) or row tile (B)
 };
 
-template <int N1, int N2, int COLS, int ROWS, bool INV, int NSTAGE, int PP = 16, bool TWD = false>
+template <int N1, int N2, int COLS, int ROWS, bool INV, int NSTAGE, int PP = 16, bool TWD = false, bool TWT = false>
 __global__ void __launch_bounds__(Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>::NT,
                                   Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>::MINB)
 k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, float2* __restrict__ ring,
@@ -459,9 +459,11 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 const int col = tid % COLS, t = tid / COLS;
                 const int n2 = d.tile * COLS + col;
                 float2 f[LPP], w0;
+                if constexpr (!TWT) {
 #pragma unroll
-                for (int i = 0; i < LPP; ++i) f[i] = W((uint32_t)n2 * (uint32_t)(TA1 << i));
-                w0 = W((uint32_t)n2 * (uint32_t)t);
+                    for (int i = 0; i < LPP; ++i) f[i] = W((uint32_t)n2 * (uint32_t)(TA1 << i));
+                    w0 = W((uint32_t)n2 * (uint32_t)t);
+                }
 #pragma unroll
                 for (int q = 0; q < PP; ++q) {
                     const float2 x = stage[(t + q * TA1) * COLS + col];
@@ -470,14 +472,21 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
 #ifndef BFFT_PIPE_NOCOMPUTE  // (experiments only: data movement without the FFT)
                 fft_engine<N1, PP>(v, t, stage, [&](int e) { return ColLayout<COLS>::at(e, col); }, tabA, bar);
 #endif
-                float2 w[PP];
-                w[0] = w0;
-                v[0] = cmul(v[0], w0);
+                if constexpr (TWT) {
+                    // W_N^{n2 k1} from the full [k1][n2] table (w_hi): one coalesced load per element
+                    const float2* wt = w_hi + (int64_t)t * N2 + n2;
 #pragma unroll
-                for (int q = 1; q < PP; ++q) {
-                    const int lb = (q & 1) ? 0 : (q & 2) ? 1 : (q & 4) ? 2 : (q & 8) ? 3 : 4;
-                    w[q] = cmul(w[q & (q - 1)], f[lb]);
-                    v[q] = cmul(v[q], w[q]);
+                    for (int q = 0; q < PP; ++q) v[q] = cmul(v[q], __ldg(wt + (int64_t)q * TA1 * N2));
+                } else {
+                    float2 w[PP];
+                    w[0] = w0;
+                    v[0] = cmul(v[0], w0);
+#pragma unroll
+                    for (int q = 1; q < PP; ++q) {
+                        const int lb = (q & 1) ? 0 : (q & 2) ? 1 : (q & 4) ? 2 : (q & 8) ? 3 : 4;
+                        w[q] = cmul(w[q & (q - 1)], f[lb]);
+                        v[q] = cmul(v[q], w[q]);
+                    }
                 }
                 float2* dst = ring + (int64_t)slot * N + n2 + (int64_t)t * N2;
 #pragma unroll

@@ -7,7 +7,8 @@
 
 using namespace bfft;
 
-template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP = 16, bool TWD = false> static PipeChoice pipe2_kernel(bool inv) {
+template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP = 16, bool TWD = false, bool TWT = false>
+static PipeChoice pipe2_kernel(bool inv) {
     using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>;
     PipeChoice ch;
     ch.n1 = N1;
@@ -17,17 +18,28 @@ template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP = 16, bool TWD 
     ch.impl = 2;
     ch.stages = NSTAGE;
     ch.boxr = CF::BOXR;
-    ch.k.fn = inv ? (const void*)&k_pipe2<N1, N2, COLS, ROWS, true, NSTAGE, PP, TWD>
-                  : (const void*)&k_pipe2<N1, N2, COLS, ROWS, false, NSTAGE, PP, TWD>;
+    ch.k.fn = inv ? (const void*)&k_pipe2<N1, N2, COLS, ROWS, true, NSTAGE, PP, TWD, TWT>
+                  : (const void*)&k_pipe2<N1, N2, COLS, ROWS, false, NSTAGE, PP, TWD, TWT>;
+    ch.twt = TWT;
     ch.pp = PP;
     ch.k.threads = CF::NT;
     ch.k.smem = CF::SMEM;
     return ch;
 }
-// radix-32 k_pipe2; TWD = direct constant-table twiddles (env BLOCKFFT_PIPE_TWD = 0/1 overrides)
-template <int N1, int N2, int COLS, int ROWS, bool TWD = false> static PipeChoice pipe2_p32(bool inv) {
-    bool twd = TWD;
+// radix-32 k_pipe2.  TWD: Stockham twiddles read directly from the constant table;
+// TWT: four-step twiddles W_N^{n2 k1} from a full [k1][n2] table (N entries, N <= 2^18).
+// Env BLOCKFFT_PIPE_TWD / BLOCKFFT_PIPE_TWT = 0/1 override the per-size defaults
+// (profiles/r01_twiddle_direct.txt, r01_twiddle_table.txt).
+template <int N1, int N2, int COLS, int ROWS, bool TWD = false, bool TWT = false>
+static PipeChoice pipe2_p32(bool inv) {
+    bool twd = TWD, twt = TWT;
     if (const char* e = getenv("BLOCKFFT_PIPE_TWD")) twd = atoi(e) != 0;
+    if (const char* e = getenv("BLOCKFFT_PIPE_TWT")) twt = atoi(e) != 0;
+    if constexpr (N1 * N2 <= (1 << 18)) {
+        if (twt)
+            return twd ? pipe2_kernel<N1, N2, COLS, ROWS, 2, 32, true, true>(inv)
+                       : pipe2_kernel<N1, N2, COLS, ROWS, 2, 32, false, true>(inv);
+    }
     return twd ? pipe2_kernel<N1, N2, COLS, ROWS, 2, 32, true>(inv) : pipe2_kernel<N1, N2, COLS, ROWS, 2, 32>(inv);
 }
 template <int N1, int N2, int COLS, int ROWS> static PipeChoice pipe2_pick(bool inv) {
@@ -65,11 +77,11 @@ PipeChoice pick_pipe(int log2n, bool inv) {
         switch (log2n) {
             case 13: return p32 ? pipe2_kernel<128, 64, 16, 32, 2, 32>(inv) : pipe2_pick<128, 64, 16, 32>(inv);
             case 14: return p32 ? pipe2_p32<128, 128, 16, 16>(inv) : pipe2_pick<128, 128, 16, 16>(inv);
-            case 15: return p32 ? pipe2_p32<256, 128, 16, 32>(inv) : pipe2_pick<256, 128, 16, 32>(inv);
+            case 15: return p32 ? pipe2_p32<256, 128, 16, 32, false, true>(inv) : pipe2_pick<256, 128, 16, 32>(inv);
             case 16:
                 if (getenv("BLOCKFFT_PIPE_TINY")) return pipe2_pick<256, 256, 8, 8>(inv);
-                // direct constant-table twiddles: +1 point here only (profiles/r01_twiddle_direct.txt)
-                return p32 ? pipe2_p32<256, 256, 16, 16, true>(inv) : pipe2_pick<256, 256, 16, 16>(inv);
+                // full four-step twiddle table (profiles/r01_twiddle_table.txt)
+                return p32 ? pipe2_p32<256, 256, 16, 16, false, true>(inv) : pipe2_pick<256, 256, 16, 16>(inv);
             case 17:
                 if (getenv("BLOCKFFT_PIPE_WIDE")) return pipe2_pick<512, 256, 16, 32>(inv);
                 return p32 ? pipe2_p32<512, 256, 8, 16>(inv) : pipe2_pick<512, 256, 8, 16>(inv);

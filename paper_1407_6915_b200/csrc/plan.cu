@@ -246,6 +246,17 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         p->kb.cols = ch.rows;
         p->pipe_impl = ch.impl;
         p->pipe_boxr = ch.boxr;
+        if (ch.twt) {
+            // full four-step twiddle table [k1][n2] = W_N^{n2 k1} (fp64 -> fp32) in tw_a
+            p->w_lb = 0;
+            for (int k1 = 0; k1 < ch.n1; ++k1)
+                for (int n2 = 0; n2 < ch.n2; ++n2) {
+                    const int64_t m = ((int64_t)n2 * k1) % n;
+                    const double ang = -2.0 * M_PI * (double)m / (double)n;
+                    ta.push_back(make_float2((float)cos(ang), (float)sin(ang)));
+                }
+            tb.push_back(make_float2(1.f, 0.f));
+        } else {
         // two-level W_N table: hi[a] = W_N^{a 2^lb}, lo[b] = W_N^b (fp64 -> fp32)
         p->w_lb = (p->log2n + 1) / 2;
         const int nhi = 1 << (p->log2n - p->w_lb), nlo = 1 << p->w_lb;
@@ -256,6 +267,7 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         for (int b = 0; b < nlo; ++b) {
             const double ang = -2.0 * M_PI * (double)b / (double)n;
             tb.push_back(make_float2((float)cos(ang), (float)sin(ang)));
+        }
         }
     } else if (variant == FFT_VARIANT_FOURSTEP) {
         if (p->log2n < 8) return bfft_set_error(FFT_E_SIZE, "unsupported transform size for four-step variant: %lld", (long long)n);

@@ -16,6 +16,7 @@ struct KernelSet {
 
 struct PipeChoice {
     int n1 = 0, n2 = 0, cols = 0, rows = 0, impl = 1, boxr = 0, stages = 0, pp = 16;
+    int twt = 0;   // 1: the kernel reads W_N^{n2 k1} from a full [k1][n2] table
     KernelSet k;
 };
 
