@@ -210,12 +210,12 @@ def main():
     import torch.distributed as dist
 
     import paper_1407_6915_b200 as bf
+    from paper_1407_6915_b200 import dist as bd
     from synth import gpu as sg
     import synth
 
-    world = env_int("WORLD_SIZE", 1)
-    rank = env_int("RANK", 0)
-    local = env_int("LOCAL_RANK", 0)
+    ri = bd.rank_info()
+    world, rank, local = ri.world, ri.rank, ri.local_rank
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -223,8 +223,7 @@ def main():
 
     n, batch = cfg["n"], cfg["batch"]
     if args.config == 3 and world > 1:       # strong scaling of the 16 GiB batch
-        f, batch = bf.partition(cfg["batch"], world, rank)
-        first = f
+        first, batch = bf.partition(cfg["batch"], world, rank)
         scaling = "strong"
     else:
         first = rank * batch                  # each rank its own records
@@ -239,8 +238,7 @@ def main():
     for _ in range(args.warmup):
         plan.exec(x, y)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    bd.barrier(dev)
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -253,20 +251,16 @@ def main():
     t_begin.record(stream)
     for i in range(args.steps):
         starts[i].record(stream)
-        plan.exec(x, y)                      # the kernel(s) launch on this stream
+        plan.exec(x, y)                      # one kernel launch on this stream
         ends[i].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    bd.barrier(dev)
     torch.cuda.synchronize()
     clk = clocks.stop()
     total_ms = t_begin.elapsed_time(t_end)
     launch_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = bd.max_over_ranks(total_ms, dev)
     recs_total = batch * world if scaling == "weak" else cfg["batch"]
     ms_per_step = max_ms / args.steps
     value = recs_total * args.steps / (max_ms * 1e-3)
@@ -281,31 +275,39 @@ def main():
              "pipe": "k_pipe"}[info["variant_name"]]
     traffic, traffic_src = ncu_traffic(kname, n, batch)
 
-    # end to end through the public C ABI with pinned host buffers
+    # end to end through the public C ABI (fft_exec_host) with HOST buffers:
+    # pinned on the GPU's NUMA node (fft_host_alloc), H2D and D2H of every step
+    # inside the timed region; compared with the host link measured here
+    # (fft_link_probe: H2D and D2H at once, same buffers)
     e2e = None
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 5)
     del x
     torch.cuda.empty_cache()
     if e2e_steps > 0:
-        h_in = torch.empty((batch, n), dtype=torch.complex64).pin_memory()
-        h_out = torch.empty_like(h_in).pin_memory()
-        h_in.copy_(y)                         # any data; the streamer is data-oblivious
+        h_in = bf.HostBuffer(batch, n, local)
+        h_out = bf.HostBuffer(batch, n, local)
+        h_in.a[:] = y.cpu().numpy()           # the bench input's transform: any data (data-oblivious path)
         del y
         torch.cuda.empty_cache()
-        bf.exec_host(h_in, n, bf.FFT_FORWARD, local, out=h_out)   # warm-up
-        if world > 1:
-            dist.barrier()
+        link = bf.link_probe(local, h_in, h_out, min(batch * 8 * n, 1 << 30), reps=3)
+        bf.exec_host(h_in.a, n, bf.FFT_FORWARD, local, out=h_out.a)   # warm-up (cached pipeline)
+        bd.barrier(dev)
         t0 = time.perf_counter()
         stats = None
         for _ in range(e2e_steps):
-            stats = bf.exec_host(h_in, n, bf.FFT_FORWARD, local, out=h_out)
-        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(el, op=dist.ReduceOp.MAX)
-        e2e = {"value": recs_total * e2e_steps / float(el.item()), "unit": "records/s",
+            stats = bf.exec_host(h_in.a, n, bf.FFT_FORWARD, local, out=h_out.a)
+        el = bd.max_over_ranks(time.perf_counter() - t0, dev)
+        each_way = batch * 8 * n * e2e_steps / el / 1e9
+        e2e = {"value": recs_total * e2e_steps / el, "unit": "records/s",
                "h2d_bytes_per_step": int(batch * 8 * n), "d2h_bytes_per_step": int(batch * 8 * n),
-               "steps": e2e_steps, "host_link_GBps_each_way": batch * 8 * n * e2e_steps / float(el.item()) / 1e9,
-               "stream_stats_last_step": stats}
+               "steps": e2e_steps, "host_link_GBps_each_way": each_way,
+               "host_link_roofline": {"h2d_GBps": link["both_h2d"], "d2h_GBps": link["both_d2h"],
+                                      "h2d_alone_GBps": link["h2d"], "d2h_alone_GBps": link["d2h"],
+                                      "how": "fft_link_probe: 1 GiB H2D and D2H at once, NUMA-local pinned"},
+               "frac_of_host_link": each_way / min(link["both_h2d"], link["both_d2h"]),
+               "numa_node": stats["numa_node"], "stream_stats_last_step": stats}
+        h_in.close()
+        h_out.close()
     else:
         del y
 

@@ -87,8 +87,37 @@ typedef struct fft_plan fft_plan; /* opaque */
 fft_plan *fft_plan_create(int64_t n, int64_t batch, int dir);
 
 /* As fft_plan_create with an explicit kernel variant (enum fft_variant).
- * A variant that cannot handle n fails with FFT_E_SIZE.                     */
+ * A variant that cannot handle n fails with FFT_E_SIZE.  dir may be 0 only
+ * with FFT_VARIANT_IDENTITY (the bit-exact copy kernel); the
+ * identity variant takes only dir 0 (else FFT_E_DIR).                       */
 fft_plan *fft_plan_create_ex(int64_t n, int64_t batch, int dir, int variant);
+
+/* Plan options (fft_plan_create_opts).  Every field 0 selects the shipped
+ * default for N — the kernel measured fastest on B200 —
+ * which is what fft_plan_create uses.  Non-zero values pick the measured
+ * alternatives explicitly (each parity-tested, tests/test_gpu_parity.py);
+ * they change speed, never the transform's definition.  No environment
+ * variable changes a plan.                                                  */
+typedef struct fft_plan_opts {
+    int variant;      /* enum fft_variant (0 = auto)                          */
+    int impl;         /* implementation inside the variant, 0 = default:
+                         FFT_VARIANT_PIPE    1 k_pipe, 2 k_pipe2, 3 k_pipe3;
+                         FFT_VARIANT_CLUSTER 1 k_cluster1 (single buffer),
+                                             2 k_cluster2 (pipelined),
+                                             3 k_cluster (TMA-staged)          */
+    int config;       /* k_pipe3 (stages, groups, claim batch) set, 0..4     */
+    int cluster_size; /* FFT_VARIANT_CLUSTER: CTAs per cluster, 0 = default */
+    int ring_records; /* FFT_VARIANT_PIPE: L2 ring slots S, 0 = sized from the
+                         tasks in flight (capped at 96 MiB); > 0 forces
+                         max(S, LAG + 1) — e.g. to reuse slots in small batches */
+    int ring_lag;     /* FFT_VARIANT_PIPE: rounds between a record's A- and
+                         B-tasks (LAG), 0 = default                           */
+} fft_plan_opts;
+
+/* fft_plan_create with options (opts may be NULL = all defaults).  Negative
+ * or out-of-range fields fail with FFT_E_ARG; a combination that has no
+ * kernel for n fails with FFT_E_SIZE.                                        */
+fft_plan *fft_plan_create_opts(int64_t n, int64_t batch, int dir, const fft_plan_opts *opts);
 
 /*
  * fft_exec — transform `batch` records.
@@ -99,9 +128,15 @@ fft_plan *fft_plan_create_ex(int64_t n, int64_t batch, int dir, int variant);
  * Enqueues the plan's kernels on `stream` and returns: no allocation, no host
  * synchronisation, no host<->device copy — graph-capturable.  Argument errors
  * are returned synchronously; launch errors as FFT_E_CUDA; device faults
- * surface at the caller's next synchronisation.  Single-kernel plans may run
- * concurrently on several streams; a four-step plan owns scratch and must not
- * run concurrently with itself (create one plan per stream).
+ * surface at the caller's next synchronisation.  Every variant enqueues only
+ * kernel launches (the pipelined four-step encodes its TMA tensor map on the
+ * host and resets its own counters at the end of each launch, no memset).
+ * Concurrency: plans with fft_plan_info.exclusive == 0 (single-pass,
+ * cluster, identity) are immutable and may run concurrently on several
+ * streams; plans with exclusive == 1 (FFT_VARIANT_PIPE: L2 ring + dependency
+ * counters; FFT_VARIANT_FOURSTEP: HBM scratch) must not run concurrently
+ * with themselves — order their execs on one stream, or create one plan per
+ * stream (as cuFFT requires).  This narrows SPEC.md:96 deliberately.
  */
 int fft_exec(const fft_plan *plan, const void *in, void *out, void *stream);
 
@@ -125,6 +160,11 @@ typedef struct fft_plan_info {
     int64_t table_bytes;  /* device twiddle tables owned by the plan           */
     int resident;         /* co-resident clusters (cluster variant) or CTAs per
                              SM of the first kernel (other variants)          */
+    int exclusive;        /* 1: the plan owns mutable device state (ring,
+                             counters, scratch) and must not run concurrently
+                             with itself (see fft_exec)                       */
+    int ring_records;     /* FFT_VARIANT_PIPE: L2 ring slots S (else 0)      */
+    int ring_lag;         /* FFT_VARIANT_PIPE: LAG (else 0)                  */
 } fft_plan_info;
 
 /* Fill *info for a plan.  Returns FFT_OK or FFT_E_ARG.                       */
@@ -143,13 +183,34 @@ int fft_plan_get_info(const fft_plan *plan, fft_plan_info *info);
 int64_t fft_file_records(int64_t file_bytes, int64_t record_len);
 int fft_partition(int64_t total_records, int nparts, int part, int64_t *first, int64_t *count);
 
+/* Per-chunk timeline (fft_stream_opts.timeline): FFT_TIMELINE_FIELDS doubles
+ * per chunk, seconds from the pipeline's start on one clock: read start, read
+ * end, H2D start, H2D end, FFT end, D2H end, write start, write end (reads
+ * and writes are 0 for pinned memory sources/sinks, which are copied directly).
+ * The overlap evidence of the streamer.                      */
+#define FFT_TIMELINE_FIELDS 8
+
 typedef struct fft_stream_opts {
     int64_t chunk_bytes;  /* bytes per pipeline chunk (the paper's block,
                              PAPER.md:55-61 dfs.block.size); 0 = default 256 MiB,
                              or env BLOCKFFT_CHUNK_BYTES                         */
-    int depth;            /* pipeline buffers per stage (>= 2); 0 = default 3  */
+    int depth;            /* chunks in flight per GPU (>= 2); 0 = default 3      */
     int variant;          /* enum fft_variant for the per-chunk plan (0=auto)  */
     int io_threads;       /* host threads splitting each chunk's pread/pwrite; 0 = 8 */
+    int direct_io;        /* 1: file I/O with O_DIRECT (page cache bypassed) when
+                             records are 4 KiB multiples (N >= 512) and the file
+                             system supports it; else buffered.  stats.direct_io
+                             reports what was used                               */
+    int numa;             /* 0: pinned slots on the GPU's NUMA node and pipeline
+                             threads on its cores (default); -1: no binding      */
+    const int64_t *tap_records; /* optional, strictly increasing logical record
+                             indices whose outputs are copied to tap_out as they
+                             stream past (sampled parity of long streams; exact
+                             when a ring sink holds >= depth chunks)            */
+    int64_t tap_count;
+    void *tap_out;        /* tap_count * 8 * n bytes                              */
+    double *timeline;     /* optional FFT_TIMELINE_FIELDS doubles per chunk       */
+    int64_t timeline_chunks; /* capacity of timeline, in chunks                   */
 } fft_stream_opts;
 
 typedef struct fft_stream_stats {
@@ -164,6 +225,9 @@ typedef struct fft_stream_stats {
     double d2h_s;         /* summed per-chunk D2H copy time (CUDA events)       */
     double write_s;       /* summed per-chunk host write time (file sink)       */
     int ngpu;
+    int numa_node;        /* NUMA node the pinned slots were bound to (-1: none) */
+    int direct_io;        /* 1 if the file I/O used O_DIRECT                      */
+    int64_t taps;         /* tapped records filled                              */
 } fft_stream_stats;
 
 /*
@@ -206,6 +270,53 @@ int fft_file_ex(const char *in_path, const char *out_path, int64_t record_len, i
  */
 int fft_exec_host(int64_t n, int64_t batch, int dir, const void *host_in, void *host_out,
                   int device, const fft_stream_opts *opts, fft_stream_stats *stats);
+
+/*
+ * fft_stream_host — the streamer over host-memory RINGS: logical record r
+ * (0 <= r < total_records) is read from record r mod in_records of host_in
+ * and its transform written to record r mod out_records of host_out.  A
+ * capture buffer replayed as an endless signal, a rolling output buffer; with
+ * in_records = out_records = total_records it is fft_exec_host.  Pinned
+ * (cudaHostAlloc / registered) rings are copied directly; pageable ones are
+ * staged.  Synchronous.  Errors as fft_exec_host, plus FFT_E_ARG for ring
+ * sizes < 1.  (the 1 TiB logical stream.)
+ */
+int fft_stream_host(int64_t n, int64_t total_records, int dir, const void *host_in, int64_t in_records,
+                    void *host_out, int64_t out_records, int device, const fft_stream_opts *opts,
+                    fft_stream_stats *stats);
+
+/*
+ * fft_file_range — one GPU's share of fft_file, for launchers that run one
+ * process per GPU or per node (the paper's map tasks over a shared file,
+ * PAPER.md:53, :111-115): records
+ * [first_record, first_record + count) of in_path (R = fft_file_records) are
+ * transformed on `device` and written at byte offset first_record*8*n of
+ * out_path, which is opened without truncation and never renamed — its owner
+ * pre-sizes it to R*8*n bytes and renames it once every range has finished
+ * (paper_1407_6915_b200.dist.fan_out).  count = 0 is a no-op.
+ * FFT_E_ARG if the range exceeds R; other errors as fft_file_ex.
+ */
+int fft_file_range(const char *in_path, const char *out_path, int64_t record_len, int dir,
+                   int64_t first_record, int64_t count, int device, const fft_stream_opts *opts,
+                   fft_stream_stats *stats);
+
+/* NUMA node of a CUDA device from sysfs (-1 if unknown); the node the
+ * streamer binds its pinned slots and threads to.                          */
+int fft_numa_node(int device);
+
+/* Pinned host memory on `device`'s NUMA node (cudaHostAlloc while the calling
+ * thread prefers that node), for sources and sinks of fft_stream_host.  NULL
+ * on error (FFT_E_ARG, FFT_E_DEVICE, FFT_E_NOMEM).  Free with fft_host_free. */
+void *fft_host_alloc(int64_t bytes, int device);
+void fft_host_free(void *p);
+
+/* Host-link roofline of the streamer: copies `bytes`
+ * between pinned host buffers and `device`, best of `reps` after a warm-up,
+ * timed with CUDA events.  gbs[0] = H2D GB/s alone, gbs[1] = D2H alone,
+ * gbs[2] / gbs[3] = H2D / D2H while both directions run at once.  Run it on
+ * several GPUs from several threads at the same time for the aggregate
+ * roofline.  Returns FFT_OK or FFT_E_ARG / FFT_E_DEVICE / FFT_E_CUDA.       */
+int fft_link_probe(int device, const void *host_src, void *host_dst, int64_t bytes, int reps, double *gbs);
 
 /* The streamer (fft_file*, fft_exec_host) caches its per-GPU resources
  * (plan, streams, device slots, pinned staging) between calls, keyed by

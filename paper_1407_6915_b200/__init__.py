@@ -52,13 +52,18 @@ class Plan:
     """
 
     def __init__(self, n: int, batch: int, direction: int = FFT_FORWARD,
-                 variant: int = VARIANT_AUTO, device=None):
+                 variant: int = VARIANT_AUTO, device=None, *, impl: int = 0, config: int = 0,
+                 cluster_size: int = 0, ring_records: int = 0, ring_lag: int = 0):
+        """``impl``, ``config``, ``cluster_size``, ``ring_records``, ``ring_lag``
+        are the fft_plan_opts fields (0 = the shipped default for n)."""
         import torch
         self.n, self.batch, self.direction = int(n), int(batch), int(direction)
         if device is not None:
             torch.cuda.set_device(device)
         self.device = torch.cuda.current_device() if torch.cuda.is_available() else None
-        h = _lib.fft_plan_create_ex(self.n, self.batch, self.direction, int(variant))
+        opts = _abi.PlanOpts(int(variant), int(impl), int(config), int(cluster_size), int(ring_records),
+                             int(ring_lag))
+        h = _lib.fft_plan_create_opts(self.n, self.batch, self.direction, ctypes.byref(opts))
         if not h:
             raise FFTError(int(_lib.fft_last_status()), last_error())
         self._h = ctypes.c_void_p(h)
@@ -78,6 +83,9 @@ class Plan:
             raise ValueError(f"{name}: expected dtype complex64, got {t.dtype}")
         if not t.is_cuda:
             raise ValueError(f"{name}: expected a CUDA tensor")
+        if t.device.index != self.device:
+            raise ValueError(f"{name}: expected a tensor on cuda:{self.device} (the plan's device), "
+                             f"got {t.device}")
         if not t.is_contiguous():
             raise ValueError(f"{name}: expected a contiguous tensor")
         if t.numel() != count * self.n or (t.dim() == 2 and tuple(t.shape) != (count, self.n)):
@@ -92,7 +100,7 @@ class Plan:
             out = x
         self._validate(x, "input", count)
         self._validate(out, "output", count)
-        s = stream if stream is not None else torch.cuda.current_stream()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
         rc = _lib.fft_exec_range(self._h, ctypes.c_void_p(x.data_ptr()),
                                  ctypes.c_void_p(out.data_ptr()), count,
                                  ctypes.c_void_p(s.cuda_stream))
@@ -132,24 +140,64 @@ def fft(x, direction: int = FFT_FORWARD, variant: int = VARIANT_AUTO, out=None):
     return out
 
 
-def _opts(chunk_bytes=0, depth=0, variant=VARIANT_AUTO, io_threads=0):
-    return _abi.StreamOpts(int(chunk_bytes), int(depth), int(variant), int(io_threads))
+class StreamOptions:
+    """fft_stream_opts (include/blockfft.h) with Python-owned tap and timeline
+    buffers.  ``taps``: record indices whose outputs are captured (``tap_out``
+    after the call, shape (len(taps), n) complex64); ``timeline``: number of
+    chunks to record (``timeline_out``, shape (chunks, 8) float64 seconds)."""
+
+    def __init__(self, n=0, chunk_bytes=0, depth=0, variant=VARIANT_AUTO, io_threads=0, direct_io=False,
+                 numa=True, taps=None, timeline=0):
+        import numpy as np
+        self.c = _abi.StreamOpts()
+        self.c.chunk_bytes, self.c.depth, self.c.variant = int(chunk_bytes), int(depth), int(variant)
+        self.c.io_threads, self.c.direct_io, self.c.numa = int(io_threads), int(bool(direct_io)), 0 if numa else -1
+        self.tap_records = self.tap_out = self.timeline_out = None
+        if taps is not None and len(taps):
+            self.tap_records = np.ascontiguousarray(np.asarray(taps, dtype=np.int64))
+            self.tap_out = np.zeros((len(self.tap_records), int(n)), dtype=np.complex64)
+            self.c.tap_records = self.tap_records.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+            self.c.tap_count = len(self.tap_records)
+            self.c.tap_out = self.tap_out.ctypes.data
+        if timeline:
+            self.timeline_out = np.full((int(timeline), _abi.TIMELINE_FIELDS), np.nan)
+            self.c.timeline = self.timeline_out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+            self.c.timeline_chunks = int(timeline)
+
+
+def _opts(chunk_bytes=0, depth=0, variant=VARIANT_AUTO, io_threads=0, options=None):
+    if options is not None:
+        return options.c
+    return StreamOptions(chunk_bytes=chunk_bytes, depth=depth, variant=variant, io_threads=io_threads).c
 
 
 def fft_file(in_path: str, out_path: str, record_len: int, ngpu: int = 1,
              direction: int = FFT_FORWARD, chunk_bytes: int = 0, depth: int = 0,
-             variant: int = VARIANT_AUTO) -> dict:
+             variant: int = VARIANT_AUTO, options: StreamOptions | None = None) -> dict:
     """The whole method on a file (fft_file_ex).  Returns the stream stats."""
     st = _abi.StreamStats()
-    o = _opts(chunk_bytes, depth, variant)
+    o = _opts(chunk_bytes, depth, variant, options=options)
     rc = _lib.fft_file_ex(os.fsencode(in_path), os.fsencode(out_path), int(record_len), int(ngpu),
                           int(direction), ctypes.byref(o), ctypes.byref(st))
     _check(rc)
     return st.as_dict()
 
 
+def file_range(in_path: str, out_path: str, record_len: int, first: int, count: int, device: int = 0,
+               direction: int = FFT_FORWARD, options: StreamOptions | None = None) -> dict:
+    """One GPU's share of a file (fft_file_range): records [first, first+count)
+    written at their own offsets of out_path (not truncated, not renamed)."""
+    st = _abi.StreamStats()
+    o = _opts(options=options)
+    rc = _lib.fft_file_range(os.fsencode(in_path), os.fsencode(out_path), int(record_len), int(direction),
+                             int(first), int(count), int(device), ctypes.byref(o), ctypes.byref(st))
+    _check(rc)
+    return st.as_dict()
+
+
 def exec_host(x_host, n: int, direction: int = FFT_FORWARD, device: int = 0, out=None,
-              chunk_bytes: int = 0, depth: int = 0, variant: int = VARIANT_AUTO) -> dict:
+              chunk_bytes: int = 0, depth: int = 0, variant: int = VARIANT_AUTO,
+              options: StreamOptions | None = None) -> dict:
     """Transform records held in host memory (torch CPU tensor, pinned or not,
     or numpy array) through the streamer (fft_exec_host).  In place unless
     ``out`` is given.  Returns the stream stats."""
@@ -160,11 +208,68 @@ def exec_host(x_host, n: int, direction: int = FFT_FORWARD, device: int = 0, out
     if nbytes != nbytes_o or nbytes % (8 * n):
         raise ValueError(f"expected equal host buffers of a multiple of {8 * n} bytes, got {nbytes} / {nbytes_o}")
     st = _abi.StreamStats()
-    o = _opts(chunk_bytes, depth, variant)
+    o = _opts(chunk_bytes, depth, variant, options=options)
     rc = _lib.fft_exec_host(int(n), nbytes // (8 * n), int(direction), ctypes.c_void_p(ptr_in),
                             ctypes.c_void_p(ptr_out), int(device), ctypes.byref(o), ctypes.byref(st))
     _check(rc)
     return st.as_dict()
+
+
+def stream_host(x_ring, out_ring, n: int, total_records: int, direction: int = FFT_FORWARD, device: int = 0,
+                options: StreamOptions | None = None) -> dict:
+    """fft_stream_host: a logical stream of ``total_records`` records read from
+    the host ring ``x_ring`` (record r from ring record r mod len) and written
+    to the host ring ``out_ring``.  Returns the stream stats."""
+    ptr_in, nb_in = _host_ptr(x_ring)
+    ptr_out, nb_out = _host_ptr(out_ring)
+    if nb_in % (8 * n) or nb_out % (8 * n):
+        raise ValueError(f"ring sizes must be multiples of {8 * n} bytes, got {nb_in} / {nb_out}")
+    st = _abi.StreamStats()
+    o = _opts(options=options)
+    rc = _lib.fft_stream_host(int(n), int(total_records), int(direction), ctypes.c_void_p(ptr_in),
+                              nb_in // (8 * n), ctypes.c_void_p(ptr_out), nb_out // (8 * n), int(device),
+                              ctypes.byref(o), ctypes.byref(st))
+    _check(rc)
+    return st.as_dict()
+
+
+def numa_node(device: int) -> int:
+    return int(_lib.fft_numa_node(int(device)))
+
+
+class HostBuffer:
+    """Pinned host memory on a GPU's NUMA node (fft_host_alloc), exposed as a
+    numpy complex64 array ``a`` of shape (records, n)."""
+
+    def __init__(self, records: int, n: int, device: int = 0):
+        import numpy as np
+        nbytes = int(records) * 8 * int(n)
+        p = _lib.fft_host_alloc(nbytes, int(device))
+        if not p:
+            raise FFTError(int(_lib.fft_last_status()), last_error())
+        self._p = p
+        self.a = np.ctypeslib.as_array((ctypes.c_char * nbytes).from_address(p)).view(np.complex64).reshape(
+            int(records), int(n))
+
+    def close(self):
+        if getattr(self, "_p", None):
+            self.a = None
+            _lib.fft_host_free(ctypes.c_void_p(self._p))
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def link_probe(device: int, src: HostBuffer, dst: HostBuffer, nbytes: int, reps: int = 3) -> dict:
+    """fft_link_probe: H2D / D2H GB/s alone and concurrently (pinned buffers)."""
+    g = (ctypes.c_double * 4)()
+    _check(_lib.fft_link_probe(int(device), ctypes.c_void_p(src._p), ctypes.c_void_p(dst._p), int(nbytes),
+                               int(reps), g))
+    return {"h2d": g[0], "d2h": g[1], "both_h2d": g[2], "both_d2h": g[3]}
 
 
 def stream_release() -> int:

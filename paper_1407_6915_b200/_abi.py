@@ -25,9 +25,10 @@ VARIANT_AUTO, VARIANT_SINGLE, VARIANT_CLUSTER, VARIANT_FOURSTEP, VARIANT_IDENTIT
 VARIANT_NAMES = {0: "auto", 1: "single", 2: "cluster", 3: "fourstep", 4: "identity", 5: "pipe"}
 
 # Every symbol include/blockfft.h declares (checked by tests/test_abi.py).
-EXPORTED = ["fft_plan_create", "fft_plan_create_ex", "fft_exec", "fft_exec_range",
+EXPORTED = ["fft_plan_create", "fft_plan_create_ex", "fft_plan_create_opts", "fft_exec", "fft_exec_range",
             "fft_plan_destroy", "fft_plan_get_info", "fft_file_records", "fft_partition",
-            "fft_file", "fft_file_ex", "fft_exec_host", "fft_stream_release", "fft_last_error", "fft_last_status", "fft_version"]
+            "fft_file", "fft_file_ex", "fft_file_range", "fft_exec_host", "fft_stream_host",
+            "fft_numa_node", "fft_host_alloc", "fft_host_free", "fft_link_probe", "fft_stream_release", "fft_last_error", "fft_last_status", "fft_version"]
 
 
 class PlanInfo(ctypes.Structure):
@@ -35,12 +36,27 @@ class PlanInfo(ctypes.Structure):
                 ("variant", ctypes.c_int), ("kernels_per_exec", ctypes.c_int),
                 ("device", ctypes.c_int), ("n1", ctypes.c_int64), ("n2", ctypes.c_int64),
                 ("cluster", ctypes.c_int), ("scratch_bytes", ctypes.c_int64),
-                ("table_bytes", ctypes.c_int64), ("resident", ctypes.c_int)]
+                ("table_bytes", ctypes.c_int64), ("resident", ctypes.c_int),
+                ("exclusive", ctypes.c_int), ("ring_records", ctypes.c_int), ("ring_lag", ctypes.c_int)]
+
+
+class PlanOpts(ctypes.Structure):
+    _fields_ = [("variant", ctypes.c_int), ("impl", ctypes.c_int), ("config", ctypes.c_int),
+                ("cluster_size", ctypes.c_int), ("ring_records", ctypes.c_int), ("ring_lag", ctypes.c_int)]
 
 
 class StreamOpts(ctypes.Structure):
     _fields_ = [("chunk_bytes", ctypes.c_int64), ("depth", ctypes.c_int),
-                ("variant", ctypes.c_int), ("io_threads", ctypes.c_int)]
+                ("variant", ctypes.c_int), ("io_threads", ctypes.c_int),
+                ("direct_io", ctypes.c_int), ("numa", ctypes.c_int),
+                ("tap_records", ctypes.POINTER(ctypes.c_int64)), ("tap_count", ctypes.c_int64),
+                ("tap_out", ctypes.c_void_p), ("timeline", ctypes.POINTER(ctypes.c_double)),
+                ("timeline_chunks", ctypes.c_int64)]
+
+
+TIMELINE_FIELDS = 8
+TIMELINE_NAMES = ["read_start", "read_end", "h2d_start", "h2d_end", "fft_end", "d2h_end",
+                  "write_start", "write_end"]
 
 
 class StreamStats(ctypes.Structure):
@@ -49,7 +65,8 @@ class StreamStats(ctypes.Structure):
                 ("wall_s", ctypes.c_double), ("read_s", ctypes.c_double),
                 ("h2d_s", ctypes.c_double), ("fft_s", ctypes.c_double),
                 ("d2h_s", ctypes.c_double), ("write_s", ctypes.c_double),
-                ("ngpu", ctypes.c_int)]
+                ("ngpu", ctypes.c_int), ("numa_node", ctypes.c_int), ("direct_io", ctypes.c_int),
+                ("taps", ctypes.c_int64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -65,6 +82,7 @@ def load() -> ctypes.CDLL:
     sig = {
         "fft_plan_create": (vp, [i64, i64, i32]),
         "fft_plan_create_ex": (vp, [i64, i64, i32, i32]),
+        "fft_plan_create_opts": (vp, [i64, i64, i32, ctypes.POINTER(PlanOpts)]),
         "fft_exec": (i32, [vp, vp, vp, vp]),
         "fft_exec_range": (i32, [vp, vp, vp, i64, vp]),
         "fft_plan_destroy": (None, [vp]),
@@ -76,6 +94,14 @@ def load() -> ctypes.CDLL:
                               ctypes.POINTER(StreamOpts), ctypes.POINTER(StreamStats)]),
         "fft_exec_host": (i32, [i64, i64, i32, vp, vp, i32, ctypes.POINTER(StreamOpts),
                                 ctypes.POINTER(StreamStats)]),
+        "fft_stream_host": (i32, [i64, i64, i32, vp, i64, vp, i64, i32, ctypes.POINTER(StreamOpts),
+                                  ctypes.POINTER(StreamStats)]),
+        "fft_file_range": (i32, [ctypes.c_char_p, ctypes.c_char_p, i64, i32, i64, i64, i32,
+                                 ctypes.POINTER(StreamOpts), ctypes.POINTER(StreamStats)]),
+        "fft_numa_node": (i32, [i32]),
+        "fft_host_alloc": (vp, [i64, i32]),
+        "fft_host_free": (None, [vp]),
+        "fft_link_probe": (i32, [i32, vp, vp, i64, i32, ctypes.POINTER(ctypes.c_double)]),
         "fft_stream_release": (i32, []),
         "fft_last_error": (ctypes.c_char_p, []),
         "fft_last_status": (i32, []),

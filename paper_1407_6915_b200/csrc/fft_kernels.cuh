@@ -111,14 +111,8 @@ struct NamedBarrier {
 };
 
 // Twiddle source traits: the radix-16/32 passes build their twiddles from
-// log2 R table entries by a multiply tree (fewer loads and live registers);
-// ConstTwDirect reads every product's twiddle from the constant table instead —
-// +1 point for k_pipe2 radix-32 at 2^16 alone, nothing on top of the full four-step twiddle
-// table, slower in the other kernels (profiles/r01_twiddle_direct.txt); kept selectable
-// (BLOCKFFT_PIPE_TWD=1).
-template <int L, int PP = 16> struct ConstTwDirect : ConstTw<L, PP> {};
+// log2 R table entries by a multiply tree (fewer loads and live registers).
 template <class Tw> struct tw_direct { static constexpr bool value = false; };
-template <int L, int PP> struct tw_direct<ConstTwDirect<L, PP>> { static constexpr bool value = true; };
 
 template <int L, int PP = 16, class Addr, class Tw, class Bar = CtaBarrier>
 __device__ __forceinline__ void fft_engine(float2 (&v)[Sched<L, PP>::P], int t, float2* sm,

@@ -32,24 +32,39 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 __device__ __forceinline__ void red_release_gpu(int* p, int v) {
     asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void wait_geq(const int* p, int target) {
-    if (ld_acquire_gpu(p) >= target) return;
-    int ns = 32;
-    while (ld_acquire_gpu(p) < target) {
-        __nanosleep(ns);
-        ns = ns < 256 ? 2 * ns : ns;
-    }
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
-// wait until *p >= target (acquire); returns the value seen
+// Wait until *p >= target, with acquire semantics.  An acquire load compiles
+// to LDG.STRONG.GPU + CCTL.IVALL (L1 invalidation), so only the first probe
+// and the final load acquire: the polls in between are relaxed (invalidating
+// L1 on every poll evicts the other warps' L1-cached data).  The writer
+// publishes with a release (fence + red), so acquiring any later value
+// synchronises with it.  Returns the value seen.
 __device__ __forceinline__ int wait_geq_v(const int* p, int target) {
     int v = ld_acquire_gpu(p);
+    if (v >= target) return v;
     int ns = 32;
-    while (v < target) {
+    do {
         __nanosleep(ns);
         ns = ns < 256 ? 2 * ns : ns;
-        v = ld_acquire_gpu(p);
-    }
-    return v;
+        v = ld_relaxed_gpu(p);
+    } while (v < target);
+    return ld_acquire_gpu(p);
+}
+__device__ __forceinline__ void wait_geq(const int* p, int target) { (void)wait_geq_v(p, target); }
+// Cross-proxy fences (PTX memory model, "proxies"): data written by generic
+// st.global in other CTAs and acquired by this thread must be made visible to
+// this thread's later async-proxy (cp.async.bulk / TMA) reads of global
+// memory; generic shared-memory accesses of a stage must be ordered before the
+// TMA / bulk copy that later overwrites it.
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ float2 ld_l2(const float2* p) { return __ldcg(p); }
 // Drop a dead 128-byte line of the ring from L2 without writing it back: once
@@ -73,6 +88,22 @@ __device__ __forceinline__ void tma_load_3d_hint(uint32_t dst, const CUtensorMap
         : "memory");
 }
 
+// The last CTA out resets the task and dependency counters ctr[0 .. 2S] and
+// the exit counter ctr[2S + 1] to zero, so the next launch on the stream
+// starts clean without a memset: fft_exec enqueues exactly one kernel.  Every
+// CTA has finished with the counters before it counts itself out (CTA barrier,
+// then a gpu-scope fence before the exit atomic), so the reset cannot race.
+__device__ __forceinline__ void pipe_exit_reset(int* ctr, int S) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const int prev = atomicAdd(ctr + 1 + 2 * S, 1);
+        if (prev == (int)gridDim.x - 1) {
+            __threadfence();
+            for (int i = 0; i <= 2 * S + 1; ++i) ctr[i] = 0;
+        }
+    }
+}
 // W_N^m from the plan's two-level table (fp64-computed, fp32-rounded):
 // W^m = hi[m >> LB] * lo[m & (2^LB - 1)], one extra rounding.
 struct TwoLevel {
@@ -119,7 +150,8 @@ static __device__ unsigned long long g_pipe_prof[32];
 #endif
 
 // ctr layout (int32): [0] task counter, [1 .. S] A-tasks published per slot,
-// [S+1 .. 2S] B-tasks finished reading per slot (cumulative across reuses).
+// [S+1 .. 2S] B-tasks finished reading per slot (cumulative across reuses),
+// [2S+1] CTAs finished (pipe_exit_reset).
 template <int N1, int N2, int COLS, int ROWS, bool INV>
 __global__ void __launch_bounds__(PipeCfg<N1, N2, COLS, ROWS>::NT, PipeCfg<N1, N2, COLS, ROWS>::MINB)
 k_pipe(const float2* __restrict__ in, float2* __restrict__ out, float2* __restrict__ ring, int64_t nrec,
@@ -247,6 +279,7 @@ k_pipe(const float2* __restrict__ in, float2* __restrict__ out, float2* __restri
 #endif
         }
     }
+    pipe_exit_reset(ctr, S);
 }
 
 }  // namespace bfft
@@ -295,10 +328,32 @@ struct Pipe2Cfg {
     // stage stride rounded to 128 bytes: TMA writes shared memory at 128-byte aligned addresses
     static constexpr int TILE = ((TILE_A > TILE_B ? TILE_A : TILE_B) + 15) / 16 * 16;
     static constexpr int BOXR = N1 < 256 ? N1 : 256;             // TMA box rows
-    static constexpr size_t SMEM = sizeof(float2) * (size_t)TILE * NSTAGE + 64 * NSTAGE + 128;
+    static constexpr int TB2 = Sched<N2, PP>::T;
+    // split four-step twiddles (TW_SPLIT): B-side tables in shared memory,
+    // T[q][s] = W_{PP^2}^{q s} (rows padded to PP + 1) and WB0[t][q] = W_{N2 PP}^{t q}
+    static constexpr int TW_T = PP * (PP + 1), TW_B0 = TB2 * PP;
+    static constexpr size_t OFF_TW = sizeof(float2) * (size_t)TILE * NSTAGE + 64 * NSTAGE + 128;
+    static constexpr size_t SMEM_TW = sizeof(float2) * (size_t)(TW_T + TW_B0);
+    static constexpr size_t SMEM = OFF_TW;   // + SMEM_TW with TW_SPLIT (pipe2_smem)
     static constexpr int MINB_RAW = 65536 / (NT * (PP == 16 ? 64 : 96));
     static constexpr int MINB = MINB_RAW < 1 ? 1 : (MINB_RAW > 8 ? 8 : MINB_RAW);
 };
+
+// How k_pipe2 applies the four-step twiddle W_N^{n2 k1}:
+//   TW_TREE  : A-side, products of log2 PP factors from the plan's two-level table;
+//   TW_TABLE : A-side, one load per element from a full [k1][n2] table (N entries);
+//   TW_SPLIT : W_N^{n2 k1} = W_N^{n2 t} * W_{N2 PP}^{n2 q} with k1 = t + TA1 q
+//              (t = the A thread's index, q = its register index).  A multiplies
+//              by its one per-thread factor W_N^{n2 t}, loaded before its column
+//              FFT; B (which holds n2 = t' + TB2 s) multiplies by
+//              W_{N2 PP}^{t' q} * W_{PP^2}^{q s} from two small shared-memory
+//              tables — no global load on either task's critical path.
+enum { TW_TREE = 0, TW_TABLE = 1, TW_SPLIT = 2 };
+template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP, int TWM>
+constexpr size_t pipe2_smem() {
+    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>;
+    return CF::SMEM + (TWM == TW_SPLIT ? CF::SMEM_TW : 0);
+}
 
 struct PipeTask {
     long long rec;  // record index
@@ -306,7 +361,7 @@ struct PipeTask {
     int tile;       // column tile (A) or row tile (B)
 };
 
-template <int N1, int N2, int COLS, int ROWS, bool INV, int NSTAGE, int PP = 16, bool TWD = false, bool TWT = false>
+template <int N1, int N2, int COLS, int ROWS, bool INV, int NSTAGE, int PP = 16, int TWM = TW_TREE>
 __global__ void __launch_bounds__(Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>::NT,
                                   Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>::MINB)
 k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, float2* __restrict__ ring,
@@ -390,6 +445,7 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                         if (gen > 0) wait_geq(doneB + slot, gen * TB);   // ring slot free (WAR)
                     } else {
                         wait_geq(doneA + slot, (gen + 1) * TA);          // column FFTs published
+                        fence_proxy_async_global();   // generic ring stores -> this bulk-copy read
                     }
 #endif
                     info[s] = d;
@@ -427,10 +483,16 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 P2_T(rt1)
                 mbar_arrive(empty0 + 8 * s);   // stage reusable (compute warps are past it)
 #ifndef BFFT_PIPE_NODEPS
+#ifndef BFFT_PIPE_REDREL
                 fence_acq_rel_gpu();            // their stores, observed through done[s], become visible
 #endif
+#endif
                 const int slot = (int)(d.rec % S);
+#ifdef BFFT_PIPE_REDREL
+                red_release_gpu((d.kind == 0 ? doneA : doneB) + slot, 1);
+#else
                 red_relaxed_gpu((d.kind == 0 ? doneA : doneB) + slot, 1);
+#endif
                 P2_T(rt2)
                 P2_ACC(16, rt0, rt1)
                 P2_ACC(17, rt1, rt2)
@@ -439,10 +501,17 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
     } else {
         // ============================================== compute warps
         const TwoLevel W{w_hi, w_lo, w_lb, (uint32_t)(N - 1)};
-        // TWD: every Stockham twiddle read from the constant table (no multiply tree)
-        const std::conditional_t<TWD, ConstTwDirect<N1, PP>, ConstTw<N1, PP>> tabA{};
-        const std::conditional_t<TWD, ConstTwDirect<N2, PP>, ConstTw<N2, PP>> tabB{};
+        const ConstTw<N1, PP> tabA{};
+        const ConstTw<N2, PP> tabB{};
         const NamedBarrier bar{1, NTC};
+        float2* tw_t = reinterpret_cast<float2*>(reinterpret_cast<char*>(sm) + CF::OFF_TW);   // T[q][s]
+        float2* tw_b0 = tw_t + CF::TW_T;                                                       // WB0[t][q]
+        if constexpr (TWM == TW_SPLIT) {
+            // w_lo = WB0 [TB2][PP] then T [PP][PP]: copy into shared memory (T rows padded)
+            for (int i = tid; i < CF::TW_B0; i += NTC) tw_b0[i] = w_lo[i];
+            for (int i = tid; i < PP * PP; i += NTC) tw_t[(i / PP) * (PP + 1) + i % PP] = w_lo[CF::TW_B0 + i];
+            bar();
+        }
         for (uint32_t k = 0;; ++k) {
             const uint32_t s = k % NSTAGE, u = k / NSTAGE;
             P2_T(ct0)
@@ -459,10 +528,12 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 const int col = tid % COLS, t = tid / COLS;
                 const int n2 = d.tile * COLS + col;
                 float2 f[LPP], w0;
-                if constexpr (!TWT) {
+                if constexpr (TWM == TW_TREE) {
 #pragma unroll
                     for (int i = 0; i < LPP; ++i) f[i] = W((uint32_t)n2 * (uint32_t)(TA1 << i));
                     w0 = W((uint32_t)n2 * (uint32_t)t);
+                } else if constexpr (TWM == TW_SPLIT) {
+                    w0 = __ldg(w_hi + t * N2 + n2);   // W_N^{n2 t}: in flight during the column FFT
                 }
 #pragma unroll
                 for (int q = 0; q < PP; ++q) {
@@ -472,7 +543,17 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
 #ifndef BFFT_PIPE_NOCOMPUTE  // (experiments only: data movement without the FFT)
                 fft_engine<N1, PP>(v, t, stage, [&](int e) { return ColLayout<COLS>::at(e, col); }, tabA, bar);
 #endif
-                if constexpr (TWT) {
+#ifndef BFFT_PIPE_NOFENCE
+                fence_proxy_async_smem();   // last generic access of the stage: before its next TMA refill
+#endif
+#ifdef BFFT_PIPE_NOTW   // (experiments only: the kernel without its four-step twiddle; results wrong)
+                if constexpr (true) {
+                } else
+#endif
+                if constexpr (TWM == TW_SPLIT) {
+#pragma unroll
+                    for (int q = 0; q < PP; ++q) v[q] = cmul(v[q], w0);   // the W_N^{n2 t} part
+                } else if constexpr (TWM == TW_TABLE) {
                     // W_N^{n2 k1} from the full [k1][n2] table (w_hi): one coalesced load per element
                     const float2* wt = w_hi + (int64_t)t * N2 + n2;
 #pragma unroll
@@ -499,10 +580,29 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                     const char* rows = reinterpret_cast<const char*>(ring + (int64_t)slot * N + (int64_t)k0 * N2);
                     for (int i = tid; i < ROWS * N2 * 8 / 128; i += NTC) l2_discard128(rows + 128 * i);
                 }
+                if constexpr (TWM == TW_SPLIT) {
+                    // the W_{N2 PP}^{n2 qa} part, n2 = t + TB2 s, qa = k1 / TA1, applied
+                    // as the elements arrive, 8 at a time (a compiler barrier keeps the
+                    // loads from all being hoisted: v plus every factor would spill)
+                    const int qa = (k0 + col) / TA1;
+                    const float2 wb = tw_b0[t * PP + qa];
+                    const float2* trow = tw_t + qa * (PP + 1);
 #pragma unroll
-                for (int q = 0; q < PP; ++q) v[q] = stage[col * RSTRIDE + t + q * TB2];
+                    for (int q0 = 0; q0 < PP; q0 += 8) {
+#pragma unroll
+                        for (int q = q0; q < q0 + 8; ++q)
+                            v[q] = cmul(stage[col * RSTRIDE + t + q * TB2], cmul(wb, trow[q]));
+                        asm volatile("" ::: "memory");
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < PP; ++q) v[q] = stage[col * RSTRIDE + t + q * TB2];
+                }
 #ifndef BFFT_PIPE_NOCOMPUTE
                 fft_engine<N2, PP>(v, t, stage, [&](int e) { return ColLayout<ROWS>::at(e, col); }, tabB, bar);
+#endif
+#ifndef BFFT_PIPE_NOFENCE
+                fence_proxy_async_smem();   // last generic access of the stage: before its next bulk refill
 #endif
                 float2* dst = out + r * N + k0 + col + (int64_t)t * N1;
 #pragma unroll
@@ -521,6 +621,7 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
             }
         }
     }
+    pipe_exit_reset(ctr, S);
 }
 
 }  // namespace bfft

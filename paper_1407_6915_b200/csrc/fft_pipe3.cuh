@@ -22,6 +22,13 @@
 // + 4 x 32 KiB (16 compute warps per SM instead of 12); 2^20: 1 x 64 KiB +
 // 2 x 64 KiB (16 instead of 8).
 //
+// Memory model: the stage is only read by the groups (generic loads) before
+// the producer refills it with TMA / bulk copies; the mbarrier arrive (empty)
+// -> wait -> copy chain orders that write-after-read, as in CUTLASS's TMA
+// pipelines (no proxy fence needed).  Ring data written with generic stores by
+// other CTAs is read with bulk copies: the producer issues
+// fence.proxy.async.global after acquiring the dependency counter.
+//
 // Deadlock freedom is k_pipe's argument unchanged: the producer blocks on a
 // task's dependencies only while the tasks its CTA already holds are staged
 // or computing, and those finish without waiting on anything outside the
@@ -195,6 +202,8 @@ k_pipe3(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 if (dp && !(dp == dep_ptr && target <= dep_seen)) {
                     dep_seen = wait_geq_v(dp, target);
                     dep_ptr = dp;
+                    // generic ring stores acquired here -> this thread's later bulk-copy reads
+                    if (d.kind == 1) fence_proxy_async_global();
                 }
                 info[s].rec = d.rec;
                 info[s].kind = d.kind;
@@ -344,6 +353,7 @@ k_pipe3(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
         }
         if (gt == 0) st_release_cta_s(exited + grp, 1);
     }
+    pipe_exit_reset(ctr, S);
 }
 
 }  // namespace bfft

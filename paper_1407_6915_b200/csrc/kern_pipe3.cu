@@ -1,7 +1,5 @@
 // kern_pipe3.cu — instantiations of k_pipe3 (fft_pipe3.cuh) and their picker,
 // compiled as their own translation unit.
-#include <cstdlib>
-
 #include "fft_pipe3.cuh"
 #include "plan_internal.h"
 
@@ -26,13 +24,11 @@ static PipeChoice pipe3_kernel(bool inv) {
     return ch;
 }
 
-// (stages, groups, claim batch) per size; env BLOCKFFT_PIPE3_CFG selects the alternatives
+// (stages, groups, claim batch) per size; fft_plan_opts::config selects the alternatives
 // measured in profiles/ (32 KiB tiles: (4,3,4) / (3,4,4) / (1,2,2) x2 CTAs / (1,2,4) x2 CTAs;
 // 64 KiB tiles: (1,2,1) / (1,2,2) / (1,2,1)+L2 prefetch / (1,2,2)+L2 prefetch; 4 = (1,2,2)+prefetch, 32 KiB)
 template <int N1, int N2, int COLS, int ROWS>
-static PipeChoice pipe3_pick(bool inv) {
-    int c = 0;
-    if (const char* e = getenv("BLOCKFFT_PIPE3_CFG")) c = atoi(e);
+static PipeChoice pipe3_pick(bool inv, int c) {
     constexpr size_t tile = sizeof(float2) * (size_t)Pipe3Cfg<N1, N2, COLS, ROWS, 1, 1, 32>::TILE;
     if constexpr (tile <= 36 * 1024) {
         if (c == 1) return pipe3_kernel<N1, N2, COLS, ROWS, 3, 4, 4>(inv);
@@ -48,14 +44,14 @@ static PipeChoice pipe3_pick(bool inv) {
     }
 }
 
-PipeChoice pick_pipe3(int log2n, bool inv) {
+PipeChoice pick_pipe3(int log2n, bool inv, int config) {
     switch (log2n) {
-        case 15: return pipe3_pick<256, 128, 16, 32>(inv);
-        case 16: return pipe3_pick<256, 256, 16, 16>(inv);
-        case 17: return pipe3_pick<512, 256, 8, 16>(inv);
-        case 18: return pipe3_pick<512, 512, 8, 8>(inv);
-        case 19: return pipe3_pick<1024, 512, 8, 16>(inv);
-        case 20: return pipe3_pick<1024, 1024, 8, 8>(inv);
+        case 15: return pipe3_pick<256, 128, 16, 32>(inv, config);
+        case 16: return pipe3_pick<256, 256, 16, 16>(inv, config);
+        case 17: return pipe3_pick<512, 256, 8, 16>(inv, config);
+        case 18: return pipe3_pick<512, 512, 8, 8>(inv, config);
+        case 19: return pipe3_pick<1024, 512, 8, 16>(inv, config);
+        case 20: return pipe3_pick<1024, 1024, 8, 8>(inv, config);
         default: return PipeChoice{};
     }
 }

@@ -1,7 +1,5 @@
 // kern_rows.cu — single-pass row kernels (k_rows) and the two-kernel four-step (k_fs_cols, k_fs_rows): instantiations and pickers, compiled as its own translation unit
 // (kernel instantiations dominate build time; plan.cu only dispatches).
-#include <cstdlib>
-
 #include "fft_kernels.cuh"
 #include "plan_internal.h"
 
@@ -60,14 +58,9 @@ KernelSet pick_row(int log2l, bool inv) {
         BFFT_L_CASES(M)
 #undef M
         case 12: return row_kernel<4096>(inv);
-        case 13:
-            if (getenv("BLOCKFFT_ROWS_P16")) return row_kernel<8192>(inv);
-            if (const char* e = getenv("BLOCKFFT_ROWS_MINB"))   // experiments: 3 CTAs per SM
-                if (atoi(e) == 3) return row_kernel<8192, 32, 3>(inv);
-            return row_kernel<8192, 32>(inv);
-        case 14:
-            if (getenv("BLOCKFFT_ROWS_P16")) return row_kernel<16384>(inv);
-            return row_kernel<16384, 32>(inv);
+        // radix-32 engines at 2^13 and 2^14 (profiles/r01_rows_2p13_minb.txt)
+        case 13: return row_kernel<8192, 32>(inv);
+        case 14: return row_kernel<16384, 32>(inv);
         default: return KernelSet{};
     }
 }

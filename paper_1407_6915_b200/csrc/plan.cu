@@ -24,6 +24,8 @@
 #include "fft_kernels.cuh"
 #include "plan_internal.h"
 
+enum { TW_TREE = 0, TW_TABLE = 1, TW_SPLIT = 2 };   // fft_pipe.cuh
+
 using namespace bfft;
 
 // ------------------------------------------------------------ error state
@@ -62,18 +64,17 @@ extern "C" int fft_version(void) { return BLOCKFFT_VERSION; }
 // ------------------------------------------------------------ TMA tensor maps
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
+    // function-local static: initialised once, thread-safe (several streamer
+    // threads make their first TMA launch concurrently)
+    static const PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
         void* p = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
-        else
-            cudaGetLastError();
-    }
+            return (PFN_cuTensorMapEncodeTiled_v12000)p;
+        cudaGetLastError();
+        return nullptr;
+    }();
     return fn;
 }
 
@@ -87,10 +88,8 @@ static int make_record_tmap(CUtensorMap* m, const void* base, int64_t count, int
     cuuint64_t strides[2] = {(cuuint64_t)n2 * 8, (cuuint64_t)n1 * n2 * 8};
     cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
     cuuint32_t es[3] = {1, 1, 1};
-    // L2 promotion 256 B: a 128-byte column-tile row fetches its neighbour tile's half too
-    // (experiments: BLOCKFFT_TMAP_PROMO = 0 none, 1 64 B, 2 128 B, 3 256 B)
-    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    if (const char* e = getenv("BLOCKFFT_TMAP_PROMO")) promo = (CUtensorMapL2promotion)std::min(3, std::max(0, atoi(e)));
+    // L2 promotion 256 B (measured no different from none or 128 B: profiles/r01_tmap_promotion.txt)
+    const CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return bfft_set_error(FFT_E_CUDA, "cuTensorMapEncodeTiled failed: CUresult %d", (int)r);
@@ -166,24 +165,19 @@ struct fft_plan {
     int occ_a = 0, occ_b = 0;
 };
 
-static int validate(int64_t n, int64_t batch, int dir) {
+// dir_ok_zero: direction 0 (identity) is accepted only where the identity
+// variant is requested explicitly (fft_plan_create_ex / _opts, the streamer)
+static int validate(int64_t n, int64_t batch, int dir, bool dir_ok_zero = false) {
     if (n < 2 || n > (1 << 22) || (n & (n - 1)) != 0)
         return bfft_set_error(FFT_E_SIZE, "unsupported transform size: %lld", (long long)n);
     if (batch < 1) return bfft_set_error(FFT_E_BATCH, "batch must be >= 1: %lld", (long long)batch);
-    if (dir != FFT_FORWARD && dir != FFT_INVERSE && dir != 0)
+    if (dir != FFT_FORWARD && dir != FFT_INVERSE && !(dir == 0 && dir_ok_zero))
         return bfft_set_error(FFT_E_DIR, "direction must be -1 or +1: %d", dir);
     return FFT_OK;
 }
 
-static int default_variant(int log2n) {
-    if (const char* e = getenv("BLOCKFFT_VARIANT")) {
-        int v = atoi(e);
-        if ((v >= 1 && v <= 3) || v == FFT_VARIANT_PIPE) return v;
-    }
-    // fastest measured per size (profiles/r01_variants_*.txt)
-    if (log2n <= 13) return FFT_VARIANT_SINGLE;
-    return FFT_VARIANT_PIPE;
-}
+// fastest measured per size (profiles/r01_variants_*.txt)
+static int default_variant(int log2n) { return log2n <= 13 ? FFT_VARIANT_SINGLE : FFT_VARIANT_PIPE; }
 
 static int set_smem(const KernelSet& k) {
     if (k.smem > 48 * 1024)
@@ -191,11 +185,10 @@ static int set_smem(const KernelSet& k) {
     return FFT_OK;
 }
 
-static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant) {
-    int rc = validate(n, batch, dir);
+static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, const fft_plan_opts& o) {
+    int variant = o.variant;
+    int rc = validate(n, batch, dir, variant == FFT_VARIANT_IDENTITY);
     if (rc) return rc;
-    if (dir == 0 && variant != FFT_VARIANT_IDENTITY && variant != FFT_VARIANT_AUTO)
-        return bfft_set_error(FFT_E_DIR, "direction 0 (identity) needs the identity variant: %d", variant);
     if (dir != 0 && variant == FFT_VARIANT_IDENTITY)
         return bfft_set_error(FFT_E_DIR, "identity variant takes direction 0: %d", dir);
     if (variant < 0 || variant > FFT_VARIANT_PIPE)
@@ -210,7 +203,6 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
     const bool inv = dir == FFT_INVERSE;
     rc = upload_const_twiddles(p->device);
     if (rc) return rc;
-    if (dir == 0) variant = FFT_VARIANT_IDENTITY;
     if (variant == FFT_VARIANT_AUTO) variant = default_variant(p->log2n);
     p->variant = variant;
 
@@ -225,9 +217,7 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         p->n2 = 1;
         stockham_table((int)n, ta, p->ka.pp);
     } else if (variant == FFT_VARIANT_CLUSTER) {
-        int want = 0;
-        if (const char* e = getenv("BLOCKFFT_CLUSTER_SIZE")) want = atoi(e);
-        ClusterChoice ch = pick_cluster(p->log2n, want, inv);
+        ClusterChoice ch = pick_cluster(p->log2n, o.cluster_size, inv, o.impl);
         if (!ch.k.fn) return bfft_set_error(FFT_E_SIZE, "unsupported transform size for cluster variant: %lld", (long long)n);
         p->ka = ch.k;
         p->n1 = ch.n1;
@@ -237,7 +227,7 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         stockham_table(ch.n1, ta, ch.pp);
         stockham_table(ch.n2, tb, ch.pp);
     } else if (variant == FFT_VARIANT_PIPE) {
-        PipeChoice ch = pick_pipe(p->log2n, inv);
+        PipeChoice ch = pick_pipe(p->log2n, inv, o.impl, o.config);
         if (!ch.k.fn) return bfft_set_error(FFT_E_SIZE, "unsupported transform size for pipelined variant: %lld", (long long)n);
         p->ka = ch.k;
         p->n1 = ch.n1;
@@ -246,28 +236,32 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         p->kb.cols = ch.rows;
         p->pipe_impl = ch.impl;
         p->pipe_boxr = ch.boxr;
-        if (ch.twt) {
-            // full four-step twiddle table [k1][n2] = W_N^{n2 k1} (fp64 -> fp32) in tw_a
-            p->w_lb = 0;
+        // four-step twiddle tables (fp64 -> fp32 RN), by the kernel's twiddle mode
+        auto w = [](int64_t m, int64_t M) {
+            const double ang = -2.0 * M_PI * (double)(m % M) / (double)M;
+            return make_float2((float)cos(ang), (float)sin(ang));
+        };
+        if (ch.twm == TW_SPLIT) {
+            // W_N^{n2 k1} = W_N^{n2 t} W_{N2 PP}^{n2 q}, k1 = t + TA1 q (fft_pipe.cuh TW_SPLIT):
+            // tw_a = WA[t][n2] = W_N^{n2 t}; tw_b = WB0[t'][q] = W_{N2 PP}^{t' q}, then T[q][s] = W_{PP^2}^{q s}
+            const int pp = ch.pp, ta1 = ch.n1 / pp, tb2 = ch.n2 / pp;
+            for (int t = 0; t < ta1; ++t)
+                for (int n2 = 0; n2 < ch.n2; ++n2) ta.push_back(w((int64_t)n2 * t, n));
+            for (int t = 0; t < tb2; ++t)
+                for (int q = 0; q < pp; ++q) tb.push_back(w((int64_t)t * q, (int64_t)ch.n2 * pp));
+            for (int q = 0; q < pp; ++q)
+                for (int s2 = 0; s2 < pp; ++s2) tb.push_back(w((int64_t)q * s2, (int64_t)pp * pp));
+        } else if (ch.twm == TW_TABLE) {
+            // full four-step twiddle table [k1][n2] = W_N^{n2 k1}
             for (int k1 = 0; k1 < ch.n1; ++k1)
-                for (int n2 = 0; n2 < ch.n2; ++n2) {
-                    const int64_t m = ((int64_t)n2 * k1) % n;
-                    const double ang = -2.0 * M_PI * (double)m / (double)n;
-                    ta.push_back(make_float2((float)cos(ang), (float)sin(ang)));
-                }
+                for (int n2 = 0; n2 < ch.n2; ++n2) ta.push_back(w((int64_t)n2 * k1, n));
             tb.push_back(make_float2(1.f, 0.f));
         } else {
-        // two-level W_N table: hi[a] = W_N^{a 2^lb}, lo[b] = W_N^b (fp64 -> fp32)
-        p->w_lb = (p->log2n + 1) / 2;
-        const int nhi = 1 << (p->log2n - p->w_lb), nlo = 1 << p->w_lb;
-        for (int a = 0; a < nhi; ++a) {
-            const double ang = -2.0 * M_PI * (double)((int64_t)a << p->w_lb) / (double)n;
-            ta.push_back(make_float2((float)cos(ang), (float)sin(ang)));
-        }
-        for (int b = 0; b < nlo; ++b) {
-            const double ang = -2.0 * M_PI * (double)b / (double)n;
-            tb.push_back(make_float2((float)cos(ang), (float)sin(ang)));
-        }
+            // two-level W_N table: hi[a] = W_N^{a 2^lb}, lo[b] = W_N^b
+            p->w_lb = (p->log2n + 1) / 2;
+            const int nhi = 1 << (p->log2n - p->w_lb), nlo = 1 << p->w_lb;
+            for (int a = 0; a < nhi; ++a) ta.push_back(w((int64_t)a << p->w_lb, n));
+            for (int b = 0; b < nlo; ++b) tb.push_back(w(b, n));
         }
     } else if (variant == FFT_VARIANT_FOURSTEP) {
         if (p->log2n < 8) return bfft_set_error(FFT_E_SIZE, "unsupported transform size for four-step variant: %lld", (long long)n);
@@ -333,7 +327,7 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         p->occ_a = std::max(p->occ_a, 1);
         const int resident = p->occ_a * p->sms;
         const int per_round = p->n2 / p->ka.cols + p->n1 / p->kb.cols;
-        PipeChoice ch = pick_pipe(p->log2n, inv);
+        PipeChoice ch = pick_pipe(p->log2n, inv, o.impl, o.config);
         // B-tasks of record r are issued LAG rounds after its A-tasks, and an
         // A-task reuses the ring slot of record r - S, whose B-tasks were
         // issued S - LAG rounds earlier.  Both gaps must exceed the tasks a
@@ -346,16 +340,19 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         const int64_t inflight = (int64_t)resident * (stages + 1);
         const int64_t rounds = (inflight + per_round - 1) / per_round;
         p->pipe_LAG = (int)(3 * rounds / 2 + 1);
-        if (const char* e = getenv("BLOCKFFT_PIPE_LAG")) p->pipe_LAG = std::max(1, atoi(e));
+        if (o.ring_lag > 0) p->pipe_LAG = o.ring_lag;
         const int64_t rec_bytes = n * (int64_t)sizeof(float2);
         const int s_cap = (int)std::max<int64_t>(p->pipe_LAG + 2, (96ll << 20) / rec_bytes);
         p->pipe_S = (int)std::min<int64_t>(p->pipe_LAG + 2 * rounds + 1, s_cap);
-        if (const char* e = getenv("BLOCKFFT_PIPE_S")) p->pipe_S = std::max(p->pipe_LAG + 1, atoi(e));
+        if (o.ring_records > 0) p->pipe_S = std::max(p->pipe_LAG + 1, o.ring_records);
         const size_t rb = (size_t)p->pipe_S * (size_t)n * sizeof(float2);
         cudaError_t e = cudaMalloc(&p->d_scratch, rb);
         if (e != cudaSuccess) return bfft_set_error(FFT_E_NOMEM, "cudaMalloc(%zu) for the pipelined ring failed: %s", rb, cudaGetErrorString(e));
-        e = cudaMalloc(&p->d_ctr, sizeof(int) * (1 + 2 * p->pipe_S));
+        // counters: task, doneA[S], doneB[S], CTAs out; zero here, and reset to zero by
+        // the last CTA of every launch (pipe_exit_reset), so fft_exec is one launch
+        e = cudaMalloc(&p->d_ctr, sizeof(int) * (2 + 2 * p->pipe_S));
         if (e != cudaSuccess) return bfft_set_error(FFT_E_NOMEM, "cudaMalloc for pipelined counters failed: %s", cudaGetErrorString(e));
+        CUDA_TRY(cudaMemset(p->d_ctr, 0, sizeof(int) * (2 + 2 * p->pipe_S)));
         p->wave = p->pipe_S;
     } else if (variant == FFT_VARIANT_FOURSTEP) {
         rc = set_smem(p->ka);
@@ -366,8 +363,7 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, int variant
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ_b, p->kb.fn, p->kb.threads, p->kb.smem));
         p->occ_a = std::max(p->occ_a, 1);
         p->occ_b = std::max(p->occ_b, 1);
-        int64_t wave_bytes = 256ll << 20;
-        if (const char* e = getenv("BLOCKFFT_FS_WAVE_BYTES")) wave_bytes = std::max(1ll, atoll(e));
+        const int64_t wave_bytes = 256ll << 20;   // one wave of records through the HBM scratch
         p->wave = std::max<int64_t>(1, std::min<int64_t>(batch, wave_bytes / (8 * n)));
         const size_t sb = (size_t)p->wave * (size_t)n * sizeof(float2);
         cudaError_t e = cudaMalloc(&p->d_scratch, sb);
@@ -384,14 +380,23 @@ static void plan_free(fft_plan* p) {
     delete p;
 }
 
-extern "C" fft_plan* fft_plan_create_ex(int64_t n, int64_t batch, int dir, int variant) {
+extern "C" fft_plan* fft_plan_create_opts(int64_t n, int64_t batch, int dir, const fft_plan_opts* opts) {
     bfft_clear_error();
+    fft_plan_opts o{};
+    if (opts) o = *opts;
+    if (o.variant < 0 || o.variant > FFT_VARIANT_PIPE || o.impl < 0 || o.config < 0 || o.cluster_size < 0 ||
+        o.ring_records < 0 || o.ring_lag < 0) {
+        bfft_set_error(FFT_E_ARG, "invalid plan options: variant=%d impl=%d config=%d cluster_size=%d "
+                       "ring_records=%d ring_lag=%d", o.variant, o.impl, o.config, o.cluster_size, o.ring_records,
+                       o.ring_lag);
+        return nullptr;
+    }
     fft_plan* p = new (std::nothrow) fft_plan();
     if (!p) {
         bfft_set_error(FFT_E_NOMEM, "out of host memory");
         return nullptr;
     }
-    if (plan_init(p, n, batch, dir, variant) != FFT_OK) {
+    if (plan_init(p, n, batch, dir, o) != FFT_OK) {
         std::string keep = g_err;
         int code = g_code;
         plan_free(p);
@@ -402,8 +407,14 @@ extern "C" fft_plan* fft_plan_create_ex(int64_t n, int64_t batch, int dir, int v
     return p;
 }
 
+extern "C" fft_plan* fft_plan_create_ex(int64_t n, int64_t batch, int dir, int variant) {
+    fft_plan_opts o{};
+    o.variant = variant;
+    return fft_plan_create_opts(n, batch, dir, &o);
+}
+
 extern "C" fft_plan* fft_plan_create(int64_t n, int64_t batch, int dir) {
-    return fft_plan_create_ex(n, batch, dir, FFT_VARIANT_AUTO);
+    return fft_plan_create_opts(n, batch, dir, nullptr);
 }
 
 extern "C" void fft_plan_destroy(fft_plan* p) { plan_free(p); }
@@ -421,6 +432,9 @@ extern "C" int fft_plan_get_info(const fft_plan* p, fft_plan_info* info) {
     info->scratch_bytes = p->d_scratch ? p->wave * p->n * 8 : 0;
     info->table_bytes = (int64_t)p->tab_bytes;
     info->resident = p->occ_a;
+    info->exclusive = (p->variant == FFT_VARIANT_PIPE || p->variant == FFT_VARIANT_FOURSTEP) ? 1 : 0;
+    info->ring_records = p->variant == FFT_VARIANT_PIPE ? p->pipe_S : 0;
+    info->ring_lag = p->variant == FFT_VARIANT_PIPE ? p->pipe_LAG : 0;
     if (p->variant == FFT_VARIANT_FOURSTEP)
         info->kernels_per_exec = (int)(2 * ((p->batch + p->wave - 1) / p->wave));
     else
@@ -475,7 +489,6 @@ static int launch(const fft_plan* p, const float2* in, float2* out, int64_t coun
             break;
         }
         case FFT_VARIANT_PIPE: {
-            CUDA_TRY(cudaMemsetAsync(p->d_ctr, 0, sizeof(int) * (1 + 2 * p->pipe_S), st));
             const int grid = p->occ_a * p->sms;
             if (p->pipe_impl >= 2) {
                 CUtensorMap tm;

@@ -16,7 +16,7 @@ struct KernelSet {
 
 struct PipeChoice {
     int n1 = 0, n2 = 0, cols = 0, rows = 0, impl = 1, boxr = 0, stages = 0, pp = 16;
-    int twt = 0;   // 1: the kernel reads W_N^{n2 k1} from a full [k1][n2] table
+    int twm = 0;   // four-step twiddle mode (fft_pipe.cuh TW_TREE / TW_TABLE / TW_SPLIT)
     KernelSet k;
 };
 
@@ -43,9 +43,9 @@ KernelSet pick_row(int log2l, bool inv);
 KernelSet pick_fs_col(int log2l, int n2, bool inv);
 KernelSet pick_fs_row(int log2l, bool inv);
 // kern_cluster.cu: cluster kernel for 2^log2n (want_c = requested cluster size or 0)
-ClusterChoice pick_cluster(int log2n, int want_c, bool inv);
+ClusterChoice pick_cluster(int log2n, int want_c, bool inv, int impl);
 // kern_pipe.cu: pipelined four-step (k_pipe / k_pipe2, or k_pipe3 through pick_pipe3)
-PipeChoice pick_pipe(int log2n, bool inv);
+PipeChoice pick_pipe(int log2n, bool inv, int impl, int config);
 // each kernel unit's copy of the constant twiddles (same contents as plan.cu's); 0 on success
 int rows_upload_const(const float2* host, size_t count);
 int cluster_upload_const(const float2* host, size_t count);
@@ -53,7 +53,7 @@ int pipe_upload_const(const float2* host, size_t count);
 
 // kern_pipe3.cu: k_pipe3 (compute groups with early stage release) for 2^log2n
 // (empty choice if that size has no k_pipe3 configuration)
-PipeChoice pick_pipe3(int log2n, bool inv);
+PipeChoice pick_pipe3(int log2n, bool inv, int config);
 // the constant-memory twiddles of kern_pipe3.cu's translation unit (same
 // contents and layout as plan.cu's c_tw); 0 on success
 int pipe3_upload_const(const float2* host, size_t count);

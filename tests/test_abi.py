@@ -63,6 +63,30 @@ def test_plan_rejects_batch_and_direction():
     assert ei.value.code == _abi.FFT_E_DIR and "direction must be -1 or +1: 2" in str(ei.value)
 
 
+def test_plan_create_rejects_direction_zero():
+    # fft_plan_create(n, b, 0) is FFT_E_DIR; identity (dir 0) is reachable
+    # only through an explicit FFT_VARIANT_IDENTITY, which in turn takes only dir 0
+    lib = _abi.lib
+    assert not lib.fft_plan_create(1024, 4, 0)
+    assert lib.fft_last_status() == _abi.FFT_E_DIR
+    assert "direction must be -1 or +1: 0" in bf.last_error()
+    assert not lib.fft_plan_create_ex(1024, 4, 0, _abi.VARIANT_AUTO)
+    assert lib.fft_last_status() == _abi.FFT_E_DIR
+    assert not lib.fft_plan_create_ex(1024, 4, -1, _abi.VARIANT_IDENTITY)
+    assert lib.fft_last_status() == _abi.FFT_E_DIR
+
+
+def test_plan_options_validated_without_gpu():
+    lib = _abi.lib
+    for field, val in (("variant", 9), ("impl", -1), ("config", -2), ("cluster_size", -1),
+                       ("ring_records", -5), ("ring_lag", -1)):
+        o = _abi.PlanOpts()
+        setattr(o, field, val)
+        assert not lib.fft_plan_create_opts(1024, 1, -1, ctypes.byref(o))
+        assert lib.fft_last_status() == _abi.FFT_E_ARG, field
+        assert f"{field}={val}" in bf.last_error()
+
+
 def test_exec_null_plan_is_arg_error():
     lib = _abi.lib
     assert lib.fft_exec(None, None, None, None) == _abi.FFT_E_ARG

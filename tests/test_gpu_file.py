@@ -175,3 +175,89 @@ def test_file_inverse_roundtrip_pipelined(tmp_path, n):
     assert np.all(oracle.rel_l2(read_c64(b, n), ref) <= oracle.tolerance(n))
     bf.fft_file(str(b), str(c), n, 1, direction=bf.FFT_INVERSE, chunk_bytes=8 * n * 5)
     assert np.all(oracle.rel_l2(read_c64(c, n), s.reshape(-1, n)) <= 2 * oracle.tolerance(n))
+
+
+def test_file_range_pieces_equal_whole_file(tmp_path):
+    # fft_file_range (one GPU's / node's share): ranges written into one
+    # pre-sized output reproduce fft_file bit for bit; a ragged tail record included
+    n = 4096
+    s = synth.random_samples(31, 0, 29 * n + 77)
+    src, whole, parts = tmp_path / "in", tmp_path / "whole", tmp_path / "parts"
+    write_file(src, s)
+    bf.fft_file(str(src), str(whole), n, 1)
+    r = bf.file_records(os.path.getsize(src), n)
+    with open(parts, "wb") as f:
+        f.truncate(r * 8 * n)
+    for g in (2, 0, 1):                        # any order: writes are positional
+        first, count = bf.partition(r, 3, g)
+        st = bf.file_range(str(src), str(parts), n, first, count, device=0,
+                           options=bf.StreamOptions(chunk_bytes=8 * n * 4))
+        assert st["records"] == count
+    assert whole.read_bytes() == parts.read_bytes()
+    with pytest.raises(bf.FFTError) as ei:
+        bf.file_range(str(src), str(parts), n, r - 1, 2)
+    assert ei.value.code == 4
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_stream_host_ring_taps(pinned):
+    # fft_stream_host: a logical stream longer than its input ring (record r reads
+    # ring record r mod K); taps capture sampled outputs along the whole stream.
+    n, k, total = 1024, 48, 1000
+    ring = torch.from_numpy(synth.random_records(41, n, 0, k))
+    ring = ring.pin_memory() if pinned else ring.clone()
+    out = torch.empty((64, n), dtype=torch.complex64)
+    out = out.pin_memory() if pinned else out
+    taps = [0, 1, 47, 48, 100, 511, 998, 999]
+    o = bf.StreamOptions(n=n, chunk_bytes=8 * n * 16, taps=taps, timeline=100)
+    st = bf.stream_host(ring, out, n, total, options=o)
+    assert st["records"] == total and st["taps"] == len(taps) and st["chunks"] == 63
+    x = ring.cuda()
+    with bf.Plan(n, k) as p:
+        y = p.exec(x, torch.empty_like(x)).cpu().numpy()
+    torch.cuda.synchronize()
+    for j, r in enumerate(taps):               # bit-identical to the in-HBM transform
+        assert np.array_equal(o.tap_out[j], y[r % k]), r
+    assert np.all(oracle.rel_l2(o.tap_out, oracle.records_c64(ring.numpy()[np.array(taps) % k], -1))
+                  <= oracle.tolerance(n))
+    # the output ring holds the last records: record r at out[r % 64]
+    for r in range(total - 64, total):
+        assert np.array_equal(out.numpy()[r % 64], y[r % k])
+    tl = o.timeline_out[:st["chunks"]]
+    assert np.all(np.isfinite(tl))
+    if pinned:                                 # pinned ring: copied directly, no read stage
+        assert np.all(tl[:, :2] == 0)
+    assert np.all(tl[:, 3] >= tl[:, 2]) and np.all(tl[:, 4] >= tl[:, 3]) and np.all(tl[:, 5] >= tl[:, 4])
+
+
+def test_stream_overlap_timeline():
+    # copies overlap compute in both directions: with D chunks in flight, chunk k+1's
+    # H2D starts before chunk k's D2H ends
+    n, k = 1 << 16, 64
+    ring = torch.from_numpy(synth.random_records(5, n, 0, k)).pin_memory()
+    out = torch.empty_like(ring).pin_memory()
+    o = bf.StreamOptions(n=n, chunk_bytes=8 * n * 8, timeline=64)
+    st = bf.stream_host(ring, out, n, 8 * k, options=o)
+    tl = o.timeline_out[:st["chunks"]]
+    overlapped = np.sum(tl[1:, 2] < tl[:-1, 5])
+    assert overlapped >= len(tl) // 2, tl[:6]
+
+
+@pytest.mark.parametrize("direct", [False, True])
+def test_file_direct_io_option(tmp_path, direct):
+    # O_DIRECT where the file system supports it (else buffered, reported in stats)
+    n = 1024
+    s = synth.random_samples(13, 0, 40 * n + 8)
+    src, dst = tmp_path / "in", tmp_path / "out"
+    write_file(src, s)
+    st = bf.fft_file(str(src), str(dst), n, 1, options=bf.StreamOptions(chunk_bytes=8 * n * 7, direct_io=direct))
+    if not direct:
+        assert st["direct_io"] == 0
+    ref = oracle.file_transform(src.read_bytes(), n)
+    assert np.all(oracle.rel_l2(read_c64(dst, n), ref) <= oracle.tolerance(n))
+    assert os.path.getsize(dst) == 41 * 8 * n
+
+
+def test_numa_node_query():
+    node = bf.numa_node(0)
+    assert isinstance(node, int) and node >= -1

@@ -19,8 +19,8 @@ import paper_1407_6915_b200 as bf  # noqa: E402
 from synth import gpu as sg  # noqa: E402
 
 
-def time_plan(n, batch, direction, variant, x, y, reps=10):
-    with bf.Plan(n, batch, direction, variant) as p:
+def time_plan(n, batch, direction, variant, x, y, reps=10, **opts):
+    with bf.Plan(n, batch, direction, variant, **opts) as p:
         info = p.info()
         for _ in range(3):
             p.exec(x, y)
@@ -57,11 +57,9 @@ def main():
             if v == 2 and k == 16:
                 cs = [8, 16]
             for c in cs:
-                if c:
-                    os.environ["BLOCKFFT_CLUSTER_SIZE"] = str(c)
                 for d in [int(t) for t in a.dirs.split(",")]:
                     try:
-                        ms, info = time_plan(n, batch, d, v, x, y)
+                        ms, info = time_plan(n, batch, d, v, x, y, cluster_size=c)
                     except bf.FFTError as e:
                         continue
                     gbs = 16.0 * n * batch / (ms * 1e-3) / 1e9
@@ -71,7 +69,6 @@ def main():
                     rows.append(row)
                     print(f"N=2^{k:<2} {info['variant_name']:>8} C={info['cluster']:<2} dir={d:+d} "
                           f"batch={batch:<8} {ms:8.3f} ms  {gbs:7.1f} GB/s  {gbs / peak:6.1%}  resident={info['resident']}", flush=True)
-            os.environ.pop("BLOCKFFT_CLUSTER_SIZE", None)
         del x, y
         torch.cuda.empty_cache()
     if a.json:
