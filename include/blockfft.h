@@ -120,6 +120,28 @@ typedef struct fft_plan_opts {
 fft_plan *fft_plan_create_opts(int64_t n, int64_t batch, int dir, const fft_plan_opts *opts);
 
 /*
+ * fft_plan_create_real — batched transform of REAL records (SURVEY.md §8(f)
+ * NEXT-1; reading c1's real reading of PAPER.md:49 "1024 ... single-precision
+ * ... 4096 bytes"): n float32 samples per record, 4 <= n <= 2^23, n a power of
+ * two (else FFT_E_SIZE); batch >= 1 (FFT_E_BATCH); dir FFT_FORWARD or
+ * FFT_INVERSE (FFT_E_DIR).
+ *   FFT_FORWARD (R2C): in = batch records of n float32 (4n bytes each), out =
+ *     the packed Hermitian half spectrum, n/2 complex64 values (4n bytes):
+ *       out[0] = (X[0], X[n/2])   (both are real for a real record)
+ *       out[k] = X[k], 0 < k < n/2   (X[n-k] = conj(X[k]) gives the rest)
+ *     with X[k] = sum_j x[j] exp(-2 pi i jk/n), unnormalised (readings c2, c3).
+ *   FFT_INVERSE (C2R): the packed half spectrum -> n real samples, x[j] =
+ *     (1/n) sum_k X[k] exp(+2 pi i jk/n) over the Hermitian-extended X.
+ * The record is read as the n/2-point complex signal x[2m] + i x[2m+1] (the
+ * same bytes), transformed by an n/2-point complex plan (any variant by
+ * size), and split / merged with W_n^k by one more kernel (csrc/real.cu).
+ * Input and output are both 4n bytes per record, so in place works and a
+ * streamed real file moves half the bytes of its complex64 promotion.
+ * fft_exec on such a plan: 16-byte aligned pointers to batch*4n bytes.
+ */
+fft_plan *fft_plan_create_real(int64_t n, int64_t batch, int dir);
+
+/*
  * fft_exec — transform `batch` records.
  *   in, out  device pointers to batch*N complex64 values, 16-byte aligned,
  *            caller-owned.  in == out (in place) is allowed; partial overlap
@@ -165,6 +187,9 @@ typedef struct fft_plan_info {
                              with itself (see fft_exec)                       */
     int ring_records;     /* FFT_VARIANT_PIPE: L2 ring slots S (else 0)      */
     int ring_lag;         /* FFT_VARIANT_PIPE: LAG (else 0)                  */
+    int real;             /* 1: a real-record plan (fft_plan_create_real); n is
+                             the real record length, the other fields describe
+                             its n/2-point complex plan                        */
 } fft_plan_info;
 
 /* Fill *info for a plan.  Returns FFT_OK or FFT_E_ARG.                       */
@@ -211,6 +236,10 @@ typedef struct fft_stream_opts {
     void *tap_out;        /* tap_count * 8 * n bytes                              */
     double *timeline;     /* optional FFT_TIMELINE_FIELDS doubles per chunk       */
     int64_t timeline_chunks; /* capacity of timeline, in chunks                   */
+    int real;             /* 1: REAL records (fft_plan_create_real): a record is n
+                             float32 samples in, n/2 packed complex64 bins out
+                             (or back, inverse), 4n bytes both ways; a file holds
+                             ceil(bytes / 4n) records (size a multiple of 4)    */
 } fft_stream_opts;
 
 typedef struct fft_stream_stats {

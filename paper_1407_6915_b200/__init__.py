@@ -127,6 +127,53 @@ class Plan:
         self.close()
 
 
+class RealPlan(Plan):
+    """Batched transform of real records (fft_plan_create_real): forward maps
+    (B, n) float32 -> (B, n/2) complex64 packed half spectra (out[:, 0] =
+    (X[0], X[n/2]), out[:, k] = X[k]); inverse maps them back, scaled by 1/n."""
+
+    def __init__(self, n: int, batch: int, direction: int = FFT_FORWARD, device=None):
+        import torch
+        self.n, self.batch, self.direction = int(n), int(batch), int(direction)
+        if device is not None:
+            torch.cuda.set_device(device)
+        self.device = torch.cuda.current_device() if torch.cuda.is_available() else None
+        h = _lib.fft_plan_create_real(self.n, self.batch, self.direction)
+        if not h:
+            raise FFTError(int(_lib.fft_last_status()), last_error())
+        self._h = ctypes.c_void_p(h)
+
+    def _check_real(self, t, name, count, real):
+        import torch
+        want = (torch.float32, self.n) if real else (torch.complex64, self.n // 2)
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{name} must be a torch.Tensor")
+        if t.dtype != want[0]:
+            raise ValueError(f"{name}: expected dtype {want[0]}, got {t.dtype}")
+        if not t.is_cuda or t.device.index != self.device:
+            raise ValueError(f"{name}: expected a tensor on cuda:{self.device}, got {t.device}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name}: expected a contiguous tensor")
+        if t.numel() != count * want[1] or (t.dim() == 2 and tuple(t.shape) != (count, want[1])):
+            raise ValueError(f"{name}: expected (B,N)=({count},{want[1]}) got {tuple(t.shape)}")
+
+    def exec(self, x, out=None, stream=None, count: int | None = None):
+        import torch
+        count = self.batch if count is None else int(count)
+        fwd = self.direction == FFT_FORWARD
+        if out is None:
+            out = torch.empty((count, self.n // 2) if fwd else (count, self.n),
+                              dtype=torch.complex64 if fwd else torch.float32, device=x.device)
+        self._check_real(x, "input", count, real=fwd)
+        self._check_real(out, "output", count, real=not fwd)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _check(_lib.fft_exec_range(self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                   count, ctypes.c_void_p(s.cuda_stream)))
+        return out
+
+    __call__ = exec
+
+
 def fft(x, direction: int = FFT_FORWARD, variant: int = VARIANT_AUTO, out=None):
     """One-shot batched FFT of a (B, N) complex64 CUDA tensor (plan per call)."""
     b, n = x.shape
@@ -147,15 +194,16 @@ class StreamOptions:
     chunks to record (``timeline_out``, shape (chunks, 8) float64 seconds)."""
 
     def __init__(self, n=0, chunk_bytes=0, depth=0, variant=VARIANT_AUTO, io_threads=0, direct_io=False,
-                 numa=True, taps=None, timeline=0):
+                 numa=True, taps=None, timeline=0, real=False):
         import numpy as np
         self.c = _abi.StreamOpts()
+        self.c.real = int(bool(real))
         self.c.chunk_bytes, self.c.depth, self.c.variant = int(chunk_bytes), int(depth), int(variant)
         self.c.io_threads, self.c.direct_io, self.c.numa = int(io_threads), int(bool(direct_io)), 0 if numa else -1
         self.tap_records = self.tap_out = self.timeline_out = None
         if taps is not None and len(taps):
             self.tap_records = np.ascontiguousarray(np.asarray(taps, dtype=np.int64))
-            self.tap_out = np.zeros((len(self.tap_records), int(n)), dtype=np.complex64)
+            self.tap_out = np.zeros((len(self.tap_records), int(n) // 2 if real else int(n)), dtype=np.complex64)
             self.c.tap_records = self.tap_records.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
             self.c.tap_count = len(self.tap_records)
             self.c.tap_out = self.tap_out.ctypes.data
@@ -205,11 +253,12 @@ def exec_host(x_host, n: int, direction: int = FFT_FORWARD, device: int = 0, out
         out = x_host
     ptr_in, nbytes = _host_ptr(x_host)
     ptr_out, nbytes_o = _host_ptr(out)
-    if nbytes != nbytes_o or nbytes % (8 * n):
-        raise ValueError(f"expected equal host buffers of a multiple of {8 * n} bytes, got {nbytes} / {nbytes_o}")
+    rb = (4 if options is not None and options.c.real else 8) * n
+    if nbytes != nbytes_o or nbytes % rb:
+        raise ValueError(f"expected equal host buffers of a multiple of {rb} bytes, got {nbytes} / {nbytes_o}")
     st = _abi.StreamStats()
     o = _opts(chunk_bytes, depth, variant, options=options)
-    rc = _lib.fft_exec_host(int(n), nbytes // (8 * n), int(direction), ctypes.c_void_p(ptr_in),
+    rc = _lib.fft_exec_host(int(n), nbytes // rb, int(direction), ctypes.c_void_p(ptr_in),
                             ctypes.c_void_p(ptr_out), int(device), ctypes.byref(o), ctypes.byref(st))
     _check(rc)
     return st.as_dict()
@@ -222,12 +271,13 @@ def stream_host(x_ring, out_ring, n: int, total_records: int, direction: int = F
     to the host ring ``out_ring``.  Returns the stream stats."""
     ptr_in, nb_in = _host_ptr(x_ring)
     ptr_out, nb_out = _host_ptr(out_ring)
-    if nb_in % (8 * n) or nb_out % (8 * n):
-        raise ValueError(f"ring sizes must be multiples of {8 * n} bytes, got {nb_in} / {nb_out}")
+    rb = (4 if options is not None and options.c.real else 8) * n
+    if nb_in % rb or nb_out % rb:
+        raise ValueError(f"ring sizes must be multiples of {rb} bytes, got {nb_in} / {nb_out}")
     st = _abi.StreamStats()
     o = _opts(options=options)
     rc = _lib.fft_stream_host(int(n), int(total_records), int(direction), ctypes.c_void_p(ptr_in),
-                              nb_in // (8 * n), ctypes.c_void_p(ptr_out), nb_out // (8 * n), int(device),
+                              nb_in // rb, ctypes.c_void_p(ptr_out), nb_out // rb, int(device),
                               ctypes.byref(o), ctypes.byref(st))
     _check(rc)
     return st.as_dict()

@@ -11,6 +11,7 @@ import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libblockfft.so")
+STRESS_LIB_PATH = os.path.join(_PKG, "libblockfft_stress.so")
 
 FFT_FORWARD = -1
 FFT_INVERSE = +1
@@ -25,7 +26,7 @@ VARIANT_AUTO, VARIANT_SINGLE, VARIANT_CLUSTER, VARIANT_FOURSTEP, VARIANT_IDENTIT
 VARIANT_NAMES = {0: "auto", 1: "single", 2: "cluster", 3: "fourstep", 4: "identity", 5: "pipe"}
 
 # Every symbol include/blockfft.h declares (checked by tests/test_abi.py).
-EXPORTED = ["fft_plan_create", "fft_plan_create_ex", "fft_plan_create_opts", "fft_exec", "fft_exec_range",
+EXPORTED = ["fft_plan_create", "fft_plan_create_ex", "fft_plan_create_opts", "fft_plan_create_real", "fft_exec", "fft_exec_range",
             "fft_plan_destroy", "fft_plan_get_info", "fft_file_records", "fft_partition",
             "fft_file", "fft_file_ex", "fft_file_range", "fft_exec_host", "fft_stream_host",
             "fft_numa_node", "fft_host_alloc", "fft_host_free", "fft_link_probe", "fft_stream_release", "fft_last_error", "fft_last_status", "fft_version"]
@@ -37,7 +38,8 @@ class PlanInfo(ctypes.Structure):
                 ("device", ctypes.c_int), ("n1", ctypes.c_int64), ("n2", ctypes.c_int64),
                 ("cluster", ctypes.c_int), ("scratch_bytes", ctypes.c_int64),
                 ("table_bytes", ctypes.c_int64), ("resident", ctypes.c_int),
-                ("exclusive", ctypes.c_int), ("ring_records", ctypes.c_int), ("ring_lag", ctypes.c_int)]
+                ("exclusive", ctypes.c_int), ("ring_records", ctypes.c_int), ("ring_lag", ctypes.c_int),
+                ("real", ctypes.c_int)]
 
 
 class PlanOpts(ctypes.Structure):
@@ -51,7 +53,7 @@ class StreamOpts(ctypes.Structure):
                 ("direct_io", ctypes.c_int), ("numa", ctypes.c_int),
                 ("tap_records", ctypes.POINTER(ctypes.c_int64)), ("tap_count", ctypes.c_int64),
                 ("tap_out", ctypes.c_void_p), ("timeline", ctypes.POINTER(ctypes.c_double)),
-                ("timeline_chunks", ctypes.c_int64)]
+                ("timeline_chunks", ctypes.c_int64), ("real", ctypes.c_int)]
 
 
 TIMELINE_FIELDS = 8
@@ -72,17 +74,20 @@ class StreamStats(ctypes.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_}
 
 
-def load() -> ctypes.CDLL:
-    if not os.path.exists(LIB_PATH):
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load a build of the library (default: the product libblockfft.so; tests
+    also load the stress build libblockfft_stress.so side by side)."""
+    if not os.path.exists(path):
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
             "(there is no CPU fallback)")
-    lib = ctypes.CDLL(LIB_PATH)
+    lib = ctypes.CDLL(path)
     vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
     sig = {
         "fft_plan_create": (vp, [i64, i64, i32]),
         "fft_plan_create_ex": (vp, [i64, i64, i32, i32]),
         "fft_plan_create_opts": (vp, [i64, i64, i32, ctypes.POINTER(PlanOpts)]),
+        "fft_plan_create_real": (vp, [i64, i64, i32]),
         "fft_exec": (i32, [vp, vp, vp, vp]),
         "fft_exec_range": (i32, [vp, vp, vp, i64, vp]),
         "fft_plan_destroy": (None, [vp]),

@@ -3,6 +3,9 @@ the GPU box with the repo snapshot).
 
   paper_1407_6915_b200/libblockfft.so  — the C-ABI product library
       csrc/plan.cu (plan layer + kernels), csrc/stream.cpp (streamer)
+  paper_1407_6915_b200/libblockfft_stress.so — TEST build: the same library with
+      the pipelined kernels compiled with -DBFFT_STRESS (random sleeps at the
+      protocol's synchronisation points; tests/test_gpu_stress.py)
   synth/libsynth.so                    — seeded CUDA fill kernel (inputs only)
 
 All CUDA code is compiled for sm_100a only:
@@ -23,6 +26,8 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 LIB = os.path.join(PKG, "libblockfft.so")
+STRESS_LIB = os.path.join(PKG, "libblockfft_stress.so")
+STRESS_UNITS = ("kern_pipe.cu", "kern_pipe3.cu")
 SYNTH_LIB = os.path.join(ROOT, "synth", "libsynth.so")
 
 
@@ -59,15 +64,22 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     headers.append(os.path.join(INC, "blockfft.h"))
     objs, cmds = [], []
     # translation units compile concurrently (each holds its own kernel instantiations)
-    for src, kind in (("plan.cu", "cu"), ("kern_rows.cu", "cu"), ("kern_cluster.cu", "cu"), ("kern_pipe.cu", "cu"),
-                      ("kern_pipe3.cu", "cu"), ("stream.cpp", "cpp")):
+    stress_objs = []
+    units = [(u, k, "") for u, k in (("plan.cu", "cu"), ("kern_rows.cu", "cu"), ("kern_cluster.cu", "cu"),
+                                     ("kern_pipe.cu", "cu"), ("kern_pipe3.cu", "cu"), ("real.cu", "cu"),
+                                     ("stream.cpp", "cpp"))]
+    units += [(u, "cu", "stress") for u in STRESS_UNITS]
+    for src, kind, flavour in units:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src + ".o")
-        objs.append(o)
+        o = os.path.join(BUILD, src + (".stress" if flavour else "") + ".o")
+        if flavour:
+            stress_objs.append(o)
+        else:
+            objs.append(o)
         if force or _newer(o, [s] + _includes(s)):
             if kind == "cu":
                 cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                       "-I", INC, "-c", s, "-o", o]
+                       "-I", INC, "-c", s, "-o", o] + (["-DBFFT_STRESS"] if flavour else [])
                 if verbose_ptxas:
                     cmd[1:1] = ["-Xptxas", "-v"]
             else:
@@ -84,6 +96,10 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     if force or _newer(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lcudart", "-lpthread"])
         os.replace(LIB + ".tmp", LIB)
+    sobjs = [o for o in objs if not any(o.endswith(u + ".o") for u in STRESS_UNITS)] + stress_objs
+    if force or _newer(STRESS_LIB, sobjs):
+        _run([NVCC, *ARCH, "-shared", "-o", STRESS_LIB + ".tmp", *sobjs, "-lcudart", "-lpthread"])
+        os.replace(STRESS_LIB + ".tmp", STRESS_LIB)
     ssrc = os.path.join(ROOT, "synth", "csrc", "synth_fill.cu")
     if force or _newer(SYNTH_LIB, [ssrc]):
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", ssrc,

@@ -149,6 +149,27 @@ static __device__ unsigned long long g_pipe_prof[32];
 #define PIPE_ACC(slot, a, b)
 #endif
 
+// Stress build (tests only: tools/stress_build.py compiles the pipelined units
+// with -DBFFT_STRESS into libblockfft_stress.so): pseudo-random sleeps of up to
+// ~2 us at the protocol's synchronisation points perturb the interleaving of
+// producers, compute warps, release warps and CTAs, so a missing wait or an
+// unordered publication shows up as a result that differs from the product
+// build's (tests/test_gpu_stress.py; compute-sanitizer is closed on this pool,
+// profiles/r02_compute_sanitizer_closed.txt).
+#ifdef BFFT_STRESS
+__device__ __forceinline__ void stress_delay(unsigned salt) {
+    const unsigned long long c = clock64();
+    unsigned h = (unsigned)(c ^ (c >> 13)) * 2654435761u ^ (blockIdx.x * 97u + salt * 131u + (threadIdx.x >> 5) * 7u);
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    h ^= h >> 15;
+    if ((h & 3u) == 0) __nanosleep((h >> 20) & 2047u);
+}
+#define BFFT_STRESS_DELAY(salt) stress_delay(salt)
+#else
+#define BFFT_STRESS_DELAY(salt)
+#endif
+
 // ctr layout (int32): [0] task counter, [1 .. S] A-tasks published per slot,
 // [S+1 .. 2S] B-tasks finished reading per slot (cumulative across reuses),
 // [2S+1] CTAs finished (pipe_exit_reset).
@@ -223,12 +244,14 @@ k_pipe(const float2* __restrict__ in, float2* __restrict__ out, float2* __restri
                 }
             }
             PIPE_T(2)
+            BFFT_STRESS_DELAY(1);
             // the slot's previous record must have been read by all its B-tasks
             if (gen > 0) {
                 if (tid == 0) wait_geq(doneB + slot, gen * TB);
                 __syncthreads();
             }
             PIPE_T(3)
+            BFFT_STRESS_DELAY(2);
             float2* dst = ring + (int64_t)slot * N + n2 + (int64_t)t * N2;
 #pragma unroll
             for (int q = 0; q < 16; ++q) dst[(int64_t)q * TA1 * N2] = v[q];
@@ -251,6 +274,7 @@ k_pipe(const float2* __restrict__ in, float2* __restrict__ out, float2* __restri
             if (tid == 0) wait_geq(doneA + slot, (gen + 1) * TA);
             __syncthreads();
             PIPE_T(5)
+            BFFT_STRESS_DELAY(3);
             const float2* src = ring + (int64_t)slot * N + (int64_t)k0 * N2;
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
@@ -263,6 +287,7 @@ k_pipe(const float2* __restrict__ in, float2* __restrict__ out, float2* __restri
                 l2_discard128(reinterpret_cast<const char*>(src) + 128 * i);  // dead intermediate: no write-back
             if (tid == 0) red_release_gpu(doneB + slot, 1);  // slot rows read: A-tasks may reuse
             PIPE_T(6)
+            BFFT_STRESS_DELAY(4);
             const int col = tid % ROWS, t = tid / ROWS;
             float2 v[16];
 #pragma unroll
@@ -434,6 +459,7 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
             const uint32_t s = k % NSTAGE, u = k / NSTAGE;
             const uint32_t fb = full0 + 8 * s;
             if (lane == 0) {
+                BFFT_STRESS_DELAY(10);
                 if (u > 0) mbar_wait(empty0 + 8 * s, (u - 1) & 1);
                 if (d.kind == 2) {
                     info[s] = d;
@@ -442,7 +468,9 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                     const int slot = (int)(d.rec % S), gen = (int)(d.rec / S);
 #ifndef BFFT_PIPE_NODEPS  // (experiments only: tools/exp measures the kernel without its waits)
                     if (d.kind == 0) {
+#ifndef BFFT_PIPE_NOWAR   // (mutation experiment only: tools/exp/stress_mutant.py)
                         if (gen > 0) wait_geq(doneB + slot, gen * TB);   // ring slot free (WAR)
+#endif
                     } else {
                         wait_geq(doneA + slot, (gen + 1) * TA);          // column FFTs published
                         fence_proxy_async_global();   // generic ring stores -> this bulk-copy read
@@ -479,8 +507,10 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 const PipeTask d = info[s];
                 if (d.kind == 2) break;
                 P2_T(rt0)
+                BFFT_STRESS_DELAY(11);
                 mbar_wait(done0 + 8 * s, u & 1);
                 P2_T(rt1)
+                BFFT_STRESS_DELAY(12);
                 mbar_arrive(empty0 + 8 * s);   // stage reusable (compute warps are past it)
 #ifndef BFFT_PIPE_NODEPS
 #ifndef BFFT_PIPE_REDREL
@@ -517,6 +547,7 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
             P2_T(ct0)
             mbar_wait(full0 + 8 * s, u & 1);
             P2_T(ct1)
+            BFFT_STRESS_DELAY(13);
             const PipeTask d = info[s];
             if (d.kind == 2) break;
             float2* stage = sm + (size_t)s * TILE;
@@ -569,6 +600,7 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                         v[q] = cmul(v[q], w[q]);
                     }
                 }
+                BFFT_STRESS_DELAY(14);
                 float2* dst = ring + (int64_t)slot * N + n2 + (int64_t)t * N2;
 #pragma unroll
                 for (int q = 0; q < PP; ++q) dst[(int64_t)q * TA1 * N2] = v[q];

@@ -190,6 +190,7 @@ k_pipe3(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
 #pragma unroll 1
                     for (int r0 = 0; r0 < N1; r0 += CF::BOXR) tma_prefetch_3d(&tmap_in, d.tile * COLS, r0, (int)d.rec);
                 }
+                BFFT_STRESS_DELAY(20);
                 if (u > 0) mbar_wait(empty0 + 8 * s, (u - 1) & 1);   // task k - NS read out of the stage
                 const int slot = (int)(d.rec % S), gen = (int)(d.rec / S);
                 const int* dp = nullptr;
@@ -252,6 +253,7 @@ k_pipe3(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                     continue;
                 }
                 ns = 32;
+                BFFT_STRESS_DELAY(22);
                 fence_acq_rel_gpu();   // the groups' stores, observed through cnt[], become visible
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
@@ -292,6 +294,7 @@ k_pipe3(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
             const long long r = info[s].rec;
             const int kind = info[s].kind, tile = info[s].tile;
             mbar_wait(full0 + 8 * s, u & 1);
+            BFFT_STRESS_DELAY(21);
             float2* stage = sm + (size_t)s * TILE;
             const int slot = (int)(r % S);
             float2 v[PP];

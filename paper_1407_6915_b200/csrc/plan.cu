@@ -163,6 +163,9 @@ struct fft_plan {
     KernelSet ka, kb;                 // kernels (kb only for four-step)
     int grid_a = 0, grid_b = 0;       // persistent/capped grid sizes (per full batch)
     int occ_a = 0, occ_b = 0;
+    int real = 0;                     // 1: real records (fft_plan_create_real), n reals each
+    fft_plan* inner = nullptr;        // real: the n/2-point complex plan
+    int rt_lb = 0;                    // real: two-level W_n split (tw_a = hi, tw_b = lo)
 };
 
 // dir_ok_zero: direction 0 (identity) is accepted only where the identity
@@ -374,6 +377,7 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, const fft_p
 
 static void plan_free(fft_plan* p) {
     if (!p) return;
+    if (p->inner) plan_free(p->inner);
     if (p->d_tab) cudaFree(p->d_tab);
     if (p->d_scratch) cudaFree(p->d_scratch);
     if (p->d_ctr) cudaFree(p->d_ctr);
@@ -417,10 +421,85 @@ extern "C" fft_plan* fft_plan_create(int64_t n, int64_t batch, int dir) {
     return fft_plan_create_opts(n, batch, dir, nullptr);
 }
 
+extern "C" fft_plan* fft_plan_create_real(int64_t n, int64_t batch, int dir) {
+    bfft_clear_error();
+    if (n < 4 || n > (1 << 23) || (n & (n - 1)) != 0) {
+        bfft_set_error(FFT_E_SIZE, "unsupported transform size: %lld", (long long)n);
+        return nullptr;
+    }
+    if (batch < 1) {
+        bfft_set_error(FFT_E_BATCH, "batch must be >= 1: %lld", (long long)batch);
+        return nullptr;
+    }
+    if (dir != FFT_FORWARD && dir != FFT_INVERSE) {
+        bfft_set_error(FFT_E_DIR, "direction must be -1 or +1: %d", dir);
+        return nullptr;
+    }
+    fft_plan* p = new (std::nothrow) fft_plan();
+    if (!p) {
+        bfft_set_error(FFT_E_NOMEM, "out of host memory");
+        return nullptr;
+    }
+    auto fail = [&]() -> fft_plan* {
+        std::string keep = g_err;
+        int code = g_code;
+        plan_free(p);
+        g_err = keep;
+        g_code = code;
+        return nullptr;
+    };
+    p->real = 1;
+    p->n = n;
+    p->batch = batch;
+    p->dir = dir;
+    p->log2n = ilog2((int)(n >> 1)) + 1;
+    p->inner = fft_plan_create_opts(n / 2, batch, dir, nullptr);
+    if (!p->inner) return fail();
+    p->device = p->inner->device;
+    p->sms = p->inner->sms;
+    p->variant = p->inner->variant;
+    // W_n^k for k <= n/4 as hi[k >> lb] * lo[k & (2^lb - 1)], fp64 -> fp32 (reading c9)
+    p->rt_lb = p->log2n / 2;
+    const int64_t nhi = ((n / 4) >> p->rt_lb) + 1, nlo = 1ll << p->rt_lb;
+    std::vector<float2> t;
+    for (int64_t a = 0; a < nhi; ++a) {
+        const double ang = -2.0 * M_PI * (double)(a << p->rt_lb) / (double)n;
+        t.push_back(make_float2((float)cos(ang), (float)sin(ang)));
+    }
+    for (int64_t b = 0; b < nlo; ++b) {
+        const double ang = -2.0 * M_PI * (double)b / (double)n;
+        t.push_back(make_float2((float)cos(ang), (float)sin(ang)));
+    }
+    p->tab_bytes = t.size() * sizeof(float2);
+    cudaError_t e = cudaMalloc(&p->d_tab, p->tab_bytes);
+    if (e != cudaSuccess) {
+        bfft_set_error(FFT_E_NOMEM, "cudaMalloc(%zu) for twiddle tables failed: %s", p->tab_bytes, cudaGetErrorString(e));
+        return fail();
+    }
+    e = cudaMemcpy(p->d_tab, t.data(), p->tab_bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        bfft_set_error(FFT_E_CUDA, "cudaMemcpy of twiddle tables failed: %s", cudaGetErrorString(e));
+        return fail();
+    }
+    p->tw_a = p->d_tab;
+    p->tw_b = p->d_tab + nhi;
+    return p;
+}
+
 extern "C" void fft_plan_destroy(fft_plan* p) { plan_free(p); }
 
 extern "C" int fft_plan_get_info(const fft_plan* p, fft_plan_info* info) {
     if (!p || !info) return bfft_set_error(FFT_E_ARG, "null plan or info pointer");
+    if (p->real) {
+        int rc = fft_plan_get_info(p->inner, info);
+        info->n = p->n;
+        info->dir = p->dir;
+        info->kernels_per_exec += 1;                 // + the split / merge kernel
+        info->table_bytes += (int64_t)p->tab_bytes;
+        info->real = 1;
+        return rc;
+    }
+    info->real = 0;
     info->n = p->n;
     info->batch = p->batch;
     info->dir = p->dir;
@@ -532,7 +611,7 @@ extern "C" int fft_exec_range(const fft_plan* p, const void* in, void* out, int6
         return bfft_set_error(FFT_E_ARG, "data pointers must be 16-byte aligned: in=%p out=%p", in, out);
     if (count < 1 || count > p->batch)
         return bfft_set_error(FFT_E_ARG, "record count out of range: expected 1..%lld, got %lld", (long long)p->batch, (long long)count);
-    const uintptr_t bytes = (uintptr_t)(count * p->n * 8);
+    const uintptr_t bytes = (uintptr_t)(count * p->n * (p->real ? 4 : 8));
     const uintptr_t a = (uintptr_t)in, b = (uintptr_t)out;
     if (a != b && a < b + bytes && b < a + bytes)
         return bfft_set_error(FFT_E_ARG, "input and output partially overlap");
@@ -540,6 +619,22 @@ extern "C" int fft_exec_range(const fft_plan* p, const void* in, void* out, int6
     CUDA_TRY(cudaGetDevice(&dev));
     if (dev != p->device)
         return bfft_set_error(FFT_E_DEVICE, "plan belongs to device %d, current device is %d", p->device, dev);
+    if (p->real) {
+        // real records: forward = complex n/2 transform, then the split in place;
+        // inverse = the merge into `out`, then the complex inverse in place
+        const int64_t h = p->n / 2;
+        cudaStream_t st = (cudaStream_t)stream;
+        if (p->dir == FFT_FORWARD) {
+            int rc = launch(p->inner, (const float2*)in, (float2*)out, count, st);
+            if (rc) return rc;
+            if (real_split_launch(false, out, out, count, h, p->tw_a, p->tw_b, p->rt_lb, p->sms, st))
+                return bfft_set_error(FFT_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+            return FFT_OK;
+        }
+        if (real_split_launch(true, in, out, count, h, p->tw_a, p->tw_b, p->rt_lb, p->sms, st))
+            return bfft_set_error(FFT_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+        return launch(p->inner, (const float2*)out, (float2*)out, count, st);
+    }
     return launch(p, (const float2*)in, (float2*)out, count, (cudaStream_t)stream);
 }
 

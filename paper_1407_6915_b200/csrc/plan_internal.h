@@ -57,3 +57,9 @@ PipeChoice pick_pipe3(int log2n, bool inv, int config);
 // the constant-memory twiddles of kern_pipe3.cu's translation unit (same
 // contents and layout as plan.cu's c_tw); 0 on success
 int pipe3_upload_const(const float2* host, size_t count);
+
+// real.cu: the real-record split (forward, in place on the n/2-point complex
+// spectrum) or merge (inverse, packed half spectrum -> Z) of h = n/2 points per
+// record; 0 on success
+int real_split_launch(bool inv, const void* in, void* out, int64_t nrec, int64_t h, const void* hi, const void* lo,
+                      int lb, int sms, cudaStream_t st);

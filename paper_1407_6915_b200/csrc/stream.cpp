@@ -351,6 +351,7 @@ struct Opts {
     char* tap_out = nullptr;
     double* timeline = nullptr;
     int64_t timeline_chunks = 0;
+    int real = 0;
 };
 
 // Runtime options of the streamer: the chunk size is the paper's one tunable
@@ -370,9 +371,13 @@ Opts resolve(const fft_stream_opts* o) {
         r.tap_out = (char*)o->tap_out;
         r.timeline = o->timeline;
         r.timeline_chunks = o->timeline ? o->timeline_chunks : 0;
+        r.real = o->real != 0;
     }
     return r;
 }
+
+// bytes per record: n complex64 (8n), or n float32 / n/2 packed complex64 (4n)
+int64_t rec_bytes(int64_t n, const Opts& o) { return o.real ? 4 * n : 8 * n; }
 
 int check_opts(const fft_stream_opts* o) {
     if (!o) return FFT_OK;
@@ -394,7 +399,7 @@ int check_opts(const fft_stream_opts* o) {
 // device.  A context is used by one call at a time; fft_stream_release()
 // frees every idle context.
 struct StreamCtx {
-    int device = 0, dir = 0, variant = 0, depth = 0, node = -1;
+    int device = 0, dir = 0, variant = 0, depth = 0, node = -1, real = 0;
     int64_t n = 0, crec = 0;
     bool stage_in = false, stage_out = false, busy = false;
     fft_plan* plan = nullptr;
@@ -443,14 +448,14 @@ int ctx_fail(StreamCtx* c, StreamCtx** out, int rc) {
                                                    cudaGetErrorString(e_)));                        \
     } while (0)
 
-int acquire_ctx(int device, int64_t n, int dir, int variant, int64_t crec, int D, bool stage_in, bool stage_out,
-                int node, StreamCtx** out) {
+int acquire_ctx(int device, int64_t n, int dir, int variant, int real, int64_t crec, int D, bool stage_in,
+                bool stage_out, int node, StreamCtx** out) {
     {
         std::lock_guard<std::mutex> g(g_ctx_mu);
         for (StreamCtx* c : g_ctx)
             if (!c->busy && c->device == device && c->n == n && c->dir == dir && c->variant == variant &&
                 c->crec == crec && c->depth == D && c->stage_in == stage_in && c->stage_out == stage_out &&
-                c->node == node) {
+                c->node == node && c->real == real) {
                 c->busy = true;
                 *out = c;
                 return FFT_OK;
@@ -467,9 +472,11 @@ int acquire_ctx(int device, int64_t n, int dir, int variant, int64_t crec, int D
     c->stage_in = stage_in;
     c->stage_out = stage_out;
     c->node = node;
+    c->real = real;
     c->busy = true;
     CKC(cudaSetDevice(device));
-    c->plan = fft_plan_create_ex(n, crec, dir, dir == 0 ? FFT_VARIANT_IDENTITY : variant);
+    c->plan = real ? fft_plan_create_real(n, crec, dir)
+                   : fft_plan_create_ex(n, crec, dir, dir == 0 ? FFT_VARIANT_IDENTITY : variant);
     if (!c->plan) {
         const int code = bfft_last_code();
         delete c;
@@ -487,7 +494,7 @@ int acquire_ctx(int device, int64_t n, int dir, int variant, int64_t crec, int D
     c->dbuf.assign(D, nullptr);
     c->hin.assign(D, nullptr);
     c->hout.assign(D, nullptr);
-    const size_t bytes = (size_t)(crec * 8 * n);
+    const size_t bytes = (size_t)(crec * (real ? 4 : 8) * n);
     NumaScope numa(node);   // pinned slots on the GPU's NUMA node (first touch happens in cudaHostAlloc)
     for (int i = 0; i < D; ++i) {
         cudaError_t e = cudaMalloc(&c->dbuf[i], bytes);
@@ -554,7 +561,7 @@ struct Progress {
 // The per-GPU pipeline over logical records [first, first+count).
 int run_pipeline(int device, int64_t n, int dir, int64_t first, int64_t count, Source* src, Sink* dst,
                  const Opts& o, fft_stream_stats* st) {
-    const int64_t rb = 8 * n;
+    const int64_t rb = rec_bytes(n, o);
     const int64_t crec = std::max<int64_t>(1, std::min<int64_t>(count, o.chunk_bytes / rb));
     const int D = o.depth;
     Span probe[2];
@@ -563,7 +570,7 @@ int run_pipeline(int device, int64_t n, int dir, int64_t first, int64_t count, S
     const int node = o.numa < 0 ? -1 : gpu_numa_node(device);
     st->numa_node = node;
     StreamCtx* c = nullptr;
-    int rc = acquire_ctx(device, n, dir, o.variant, crec, D, stage_in, stage_out, node, &c);
+    int rc = acquire_ctx(device, n, dir, o.variant, o.real, crec, D, stage_in, stage_out, node, &c);
     if (rc) return rc;
     const int64_t nchunks = (count + crec - 1) / crec;
     auto chunk_first = [&](int64_t k) { return first + k * crec; };
@@ -775,12 +782,22 @@ int run_pipeline(int device, int64_t n, int dir, int64_t first, int64_t count, S
     return rc;
 }
 
-int check_n_dir(int64_t n, int dir) {
-    if (n < 2 || n > (1 << 22) || (n & (n - 1)))
+int check_n_dir(int64_t n, int dir, bool real) {
+    if ((real ? (n < 4 || n > (1 << 23)) : (n < 2 || n > (1 << 22))) || (n & (n - 1)))
         return bfft_set_error(FFT_E_SIZE, "unsupported transform size: %lld", (long long)n);
-    if (dir != FFT_FORWARD && dir != FFT_INVERSE && dir != 0)
-        return bfft_set_error(FFT_E_DIR, "direction must be -1, +1 or 0 (identity): %d", dir);
+    if (dir != FFT_FORWARD && dir != FFT_INVERSE && (dir != 0 || real))
+        return bfft_set_error(FFT_E_DIR, real ? "direction must be -1 or +1: %d"
+                                              : "direction must be -1, +1 or 0 (identity): %d", dir);
     return FFT_OK;
+}
+
+// records of a file: ceil(size / record bytes), the final one zero-padded (reading c6)
+int64_t file_records_of(int64_t size, int64_t n, const Opts& o) {
+    if (!o.real) return fft_file_records(size, n);
+    if (size % 4)
+        return -bfft_set_error(FFT_E_ARG, "file size %lld is not a multiple of 4 bytes", (long long)size);
+    if (size == 0) return -bfft_set_error(FFT_E_EMPTY, "empty input");
+    return (size + 4 * n - 1) / (4 * n);
 }
 
 int check_device(int device) {
@@ -795,7 +812,7 @@ int check_device(int device) {
 }
 
 // O_DIRECT needs 4 KiB-aligned offsets and lengths: records of 8N bytes with N >= 512.
-bool direct_ok(const Opts& o, int64_t n) { return o.direct_io && (8 * n) % 4096 == 0; }
+bool direct_ok(const Opts& o, int64_t n) { return o.direct_io && rec_bytes(n, o) % 4096 == 0; }
 
 int open_input(const char* path, bool od, int* fd, int* fd_direct, int64_t* size) {
     *fd = open(path, O_RDONLY);
@@ -818,7 +835,8 @@ extern "C" int fft_stream_host(int64_t n, int64_t total_records, int dir, const 
                                fft_stream_stats* stats) {
     bfft_clear_error();
     if (!host_in || !host_out) return bfft_set_error(FFT_E_ARG, "null host pointer");
-    int rc = check_n_dir(n, dir);
+    const bool real = opts && opts->real;
+    int rc = check_n_dir(n, dir, real);
     if (rc) return rc;
     if (total_records < 1) return bfft_set_error(FFT_E_BATCH, "batch must be >= 1: %lld", (long long)total_records);
     if (in_records < 1 || out_records < 1)
@@ -826,8 +844,8 @@ extern "C" int fft_stream_host(int64_t n, int64_t total_records, int dir, const 
                               (long long)in_records, (long long)out_records);
     if ((rc = check_opts(opts)) || (rc = check_device(device))) return rc;
     const Opts o = resolve(opts);
-    MemSource src(host_in, in_records, 8 * n, is_pinned(host_in));
-    MemSink dst(host_out, out_records, 8 * n, is_pinned(host_out));
+    MemSource src(host_in, in_records, rec_bytes(n, o), is_pinned(host_in));
+    MemSink dst(host_out, out_records, rec_bytes(n, o), is_pinned(host_out));
     fft_stream_stats st{};
     st.numa_node = -1;
     const double t0 = now_s();
@@ -847,7 +865,7 @@ extern "C" int fft_file_ex(const char* in_path, const char* out_path, int64_t n,
                            const fft_stream_opts* opts, fft_stream_stats* stats) {
     bfft_clear_error();
     if (!in_path || !out_path) return bfft_set_error(FFT_E_ARG, "null path");
-    int rc = check_n_dir(n, dir);
+    int rc = check_n_dir(n, dir, opts && opts->real);
     if (rc) return rc;
     if ((rc = check_opts(opts))) return rc;
     int ndev = 0;
@@ -861,7 +879,8 @@ extern "C" int fft_file_ex(const char* in_path, const char* out_path, int64_t n,
     int fd = -1, fdd = -1;
     int64_t size = 0;
     if ((rc = open_input(in_path, od, &fd, &fdd, &size))) return rc;
-    const int64_t R = fft_file_records(size, n);
+    const int64_t R = file_records_of(size, n, o);
+    const int64_t rb = rec_bytes(n, o);
     if (R < 0) {
         close(fd);
         if (fdd >= 0) close(fdd);
@@ -875,7 +894,7 @@ extern "C" int fft_file_ex(const char* in_path, const char* out_path, int64_t n,
         return bfft_set_error(FFT_E_IO, "cannot create %s: %s", tmp.c_str(), strerror(errno));
     }
     const int ofdd = od ? open(tmp.c_str(), O_WRONLY | O_DIRECT) : -1;
-    const int64_t out_bytes = R * 8 * n;
+    const int64_t out_bytes = R * rb;
     if (ftruncate(ofd, out_bytes) != 0)
         rc = bfft_set_error(FFT_E_IO, "cannot size %s to %lld bytes: %s", tmp.c_str(), (long long)out_bytes,
                             strerror(errno));
@@ -891,8 +910,8 @@ extern "C" int fft_file_ex(const char* in_path, const char* out_path, int64_t n,
                 int64_t first = 0, count = 0;
                 fft_partition(R, ngpu, g, &first, &count);
                 if (count == 0) return;
-                FileSource src(fdd >= 0 ? fdd : fd, size, 8 * n, in_path, o.io_threads, fdd >= 0);
-                FileSink dst(ofdd >= 0 ? ofdd : ofd, 8 * n, tmp.c_str(), o.io_threads);
+                FileSource src(fdd >= 0 ? fdd : fd, size, rb, in_path, o.io_threads, fdd >= 0);
+                FileSink dst(ofdd >= 0 ? ofdd : ofd, rb, tmp.c_str(), o.io_threads);
                 fft_stream_stats st{};
                 st.direct_io = fdd >= 0 && ofdd >= 0;
                 rcs[g] = run_pipeline(g, n, dir, first, count, &src, &dst, o, &st);
@@ -926,7 +945,7 @@ extern "C" int fft_file_range(const char* in_path, const char* out_path, int64_t
                               int64_t count, int device, const fft_stream_opts* opts, fft_stream_stats* stats) {
     bfft_clear_error();
     if (!in_path || !out_path) return bfft_set_error(FFT_E_ARG, "null path");
-    int rc = check_n_dir(n, dir);
+    int rc = check_n_dir(n, dir, opts && opts->real);
     if (rc) return rc;
     if ((rc = check_opts(opts))) return rc;
     const Opts o = resolve(opts);
@@ -934,7 +953,8 @@ extern "C" int fft_file_range(const char* in_path, const char* out_path, int64_t
     int fd = -1, fdd = -1;
     int64_t size = 0;
     if ((rc = open_input(in_path, od, &fd, &fdd, &size))) return rc;
-    const int64_t R = fft_file_records(size, n);
+    const int64_t R = file_records_of(size, n, o);
+    const int64_t rb = rec_bytes(n, o);
     auto done = [&](int code) {
         close(fd);
         if (fdd >= 0) close(fdd);
@@ -958,8 +978,8 @@ extern "C" int fft_file_range(const char* in_path, const char* out_path, int64_t
     const int ofd = open(out_path, O_WRONLY | O_CREAT, 0644);
     if (ofd < 0) return done(bfft_set_error(FFT_E_IO, "cannot open %s: %s", out_path, strerror(errno)));
     const int ofdd = od ? open(out_path, O_WRONLY | O_DIRECT) : -1;
-    FileSource src(fdd >= 0 ? fdd : fd, size, 8 * n, in_path, o.io_threads, fdd >= 0);
-    FileSink dst(ofdd >= 0 ? ofdd : ofd, 8 * n, out_path, o.io_threads);
+    FileSource src(fdd >= 0 ? fdd : fd, size, rb, in_path, o.io_threads, fdd >= 0);
+    FileSink dst(ofdd >= 0 ? ofdd : ofd, rb, out_path, o.io_threads);
     st.direct_io = fdd >= 0 && ofdd >= 0;
     const double t0 = now_s();
     rc = run_pipeline(device, n, dir, first_record, count, &src, &dst, o, &st);
