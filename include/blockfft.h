@@ -142,6 +142,24 @@ fft_plan *fft_plan_create_opts(int64_t n, int64_t batch, int dir, const fft_plan
 fft_plan *fft_plan_create_real(int64_t n, int64_t batch, int dir);
 
 /*
+ * fft_plan_create_stft — overlapping records: the short-time Fourier
+ * transform of a complex64 signal (the
+ * paper's future work).  Frame f (0 <= f < frames) is the n samples starting
+ * at sample f*hop, multiplied by window[0..n) (host pointer, n float32,
+ * copied into the plan; NULL = rectangular):
+ *   out[f][k] = sum_j window[j] in[f*hop + j] exp(-+2 pi i jk/n)   (dir as in
+ *   fft_plan_create; FFT_INVERSE scales by 1/n per frame).
+ * hop >= 1 (hop < n overlaps frames, hop == n is the record transform, hop > n
+ * skips samples), else FFT_E_ARG; n, frames, dir as in fft_plan_create.
+ * fft_exec(plan, in, out, stream): in = the signal, (frames-1)*hop + n
+ * complex64 samples; out = frames*n complex64; in and out must not overlap.
+ * Frames of up to 2^13 points are framed and windowed on load by the
+ * single-pass kernel (one launch); longer frames are framed into out by one
+ * more kernel and transformed in place.
+ */
+fft_plan *fft_plan_create_stft(int64_t n, int64_t hop, int64_t frames, int dir, const float *window);
+
+/*
  * fft_exec — transform `batch` records.
  *   in, out  device pointers to batch*N complex64 values, 16-byte aligned,
  *            caller-owned.  in == out (in place) is allowed; partial overlap
@@ -190,6 +208,8 @@ typedef struct fft_plan_info {
     int real;             /* 1: a real-record plan (fft_plan_create_real); n is
                              the real record length, the other fields describe
                              its n/2-point complex plan                        */
+    int64_t hop;          /* STFT plan (fft_plan_create_stft): samples between
+                             frames (else 0)                                   */
 } fft_plan_info;
 
 /* Fill *info for a plan.  Returns FFT_OK or FFT_E_ARG.                       */
@@ -240,6 +260,15 @@ typedef struct fft_stream_opts {
                              float32 samples in, n/2 packed complex64 bins out
                              (or back, inverse), 4n bytes both ways; a file holds
                              ceil(bytes / 4n) records (size a multiple of 4)    */
+    int64_t hop;          /* > 0: STFT (fft_plan_create_stft) of the file's
+                             complex64 signal of L samples: F = 1 + ceil((L-n)/hop)
+                             frames (L <= n: 1), samples past L read as zero;
+                             output F*n complex64.  Each chunk reads its frames'
+                             samples including the n - hop halo it shares with
+                             the next chunk or GPU (re-read, no exchange).  Files
+                             only (fft_file_ex, fft_file_range)                 */
+    const float *window;  /* STFT window, window_len = n floats (NULL = none)  */
+    int64_t window_len;
 } fft_stream_opts;
 
 typedef struct fft_stream_stats {
@@ -352,6 +381,31 @@ int fft_link_probe(int device, const void *host_src, void *host_dst, int64_t byt
  * (device, n, dir, variant, chunk records, depth); fft_stream_release frees
  * every cached set not in use and returns how many it freed.              */
 int fft_stream_release(void);
+
+/*
+ * One transform larger than a GPU (the out-of-card /
+ * GPU-cluster FFTs of PAPER.md:41, :43): ONE record of n complex64 points held
+ * as ngpu contiguous slabs, GPU g owning points [g n/ngpu, (g+1) n/ngpu).
+ * fft_dplan_create: n a power of two, 4 <= n <= 2^44, n = n1 n2 with n1 =
+ * 2^ceil(log2(n)/2) <= 2^22 and n1, n2 multiples of ngpu (else FFT_E_SIZE);
+ * ngpu a power of two <= device count whose GPUs can all reach each other as
+ * peers (NVLink / NVSwitch), else FFT_E_DEVICE; devices = the ngpu CUDA device
+ * ids (NULL = 0..ngpu-1); dir FFT_FORWARD / FFT_INVERSE (1/n).  Owns per GPU
+ * two scratch slabs (2 n/ngpu complex64), twiddle tables and two batched plans.
+ * fft_dplan_exec: slabs_in[g] / slabs_out[g] = device pointers on GPU g of
+ * n/ngpu complex64 (16-byte aligned; out may equal in).  Distributed
+ * four-step: three transposes, each ONE kernel per GPU that applies the
+ * step's twiddle and stores every element straight into the peer GPU's buffer
+ * over NVLink (the all-to-all fused with the arithmetic; no NCCL), with the
+ * column and row FFTs between them.  Output slabs are in natural order.
+ * Synchronous (returns when every output slab is written); not concurrent
+ * with itself.  fft_dplan_geometry reports (n1, n2, ngpu).
+ */
+typedef struct fft_dplan fft_dplan;
+fft_dplan *fft_dplan_create(int64_t n, int ngpu, const int *devices, int dir);
+int fft_dplan_exec(fft_dplan *plan, void *const *slabs_in, void *const *slabs_out);
+int fft_dplan_geometry(const fft_dplan *plan, int64_t *n1, int64_t *n2, int *ngpu);
+void fft_dplan_destroy(fft_dplan *plan);
 
 /* Thread-local message describing the last error on this thread ("" if none). */
 const char *fft_last_error(void);

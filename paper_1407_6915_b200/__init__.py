@@ -174,6 +174,98 @@ class RealPlan(Plan):
     __call__ = exec
 
 
+class StftPlan(Plan):
+    """Short-time Fourier transform (fft_plan_create_stft): ``frames`` frames of
+    n samples every ``hop`` samples of a complex64 signal, times an optional
+    real window; exec(signal, out) with signal of (frames-1)*hop + n samples
+    and out (frames, n)."""
+
+    def __init__(self, n: int, hop: int, frames: int, direction: int = FFT_FORWARD, window=None, device=None):
+        import numpy as np
+        import torch
+        self.n, self.batch, self.direction, self.hop = int(n), int(frames), int(direction), int(hop)
+        if device is not None:
+            torch.cuda.set_device(device)
+        self.device = torch.cuda.current_device() if torch.cuda.is_available() else None
+        w = None
+        if window is not None:
+            self._win = np.ascontiguousarray(np.asarray(window, dtype=np.float32))
+            if self._win.shape != (self.n,):
+                raise ValueError(f"window: expected ({self.n},) got {self._win.shape}")
+            w = self._win.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+        h = _lib.fft_plan_create_stft(self.n, self.hop, self.batch, self.direction, w)
+        if not h:
+            raise FFTError(int(_lib.fft_last_status()), last_error())
+        self._h = ctypes.c_void_p(h)
+
+    def exec(self, x, out=None, stream=None, count: int | None = None):
+        import torch
+        count = self.batch if count is None else int(count)
+        need = (count - 1) * self.hop + self.n
+        if x.dtype != torch.complex64 or not x.is_cuda or not x.is_contiguous() or x.numel() < need:
+            raise ValueError(f"input: expected a contiguous complex64 CUDA signal of >= {need} samples")
+        if out is None:
+            out = torch.empty((count, self.n), dtype=torch.complex64, device=x.device)
+        self._validate(out, "output", count)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _check(_lib.fft_exec_range(self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                   count, ctypes.c_void_p(s.cuda_stream)))
+        return out
+
+    __call__ = exec
+
+
+class DistPlan:
+    """One record larger than a GPU (fft_dplan_create): n complex64 points as
+    ``ngpu`` contiguous slabs, slab g on device ``devices[g]``; exec(slabs_in,
+    slabs_out) transforms in natural order (synchronous)."""
+
+    def __init__(self, n: int, ngpu: int, direction: int = FFT_FORWARD, devices=None):
+        self.n, self.ngpu, self.direction = int(n), int(ngpu), int(direction)
+        self.devices = list(devices) if devices is not None else list(range(self.ngpu))
+        arr = (ctypes.c_int * self.ngpu)(*self.devices)
+        h = _lib.fft_dplan_create(self.n, self.ngpu, arr, self.direction)
+        if not h:
+            raise FFTError(int(_lib.fft_last_status()), last_error())
+        self._h = ctypes.c_void_p(h)
+
+    def geometry(self) -> tuple[int, int]:
+        n1, n2, g = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+        _check(_lib.fft_dplan_geometry(self._h, ctypes.byref(n1), ctypes.byref(n2), ctypes.byref(g)))
+        return n1.value, n2.value
+
+    def exec(self, slabs_in, slabs_out=None):
+        import torch
+        slabs_out = slabs_in if slabs_out is None else slabs_out
+        per = self.n // self.ngpu
+        for g, (a, b) in enumerate(zip(slabs_in, slabs_out)):
+            for t in (a, b):
+                if t.dtype != torch.complex64 or not t.is_contiguous() or t.numel() != per or \
+                        t.device != torch.device("cuda", self.devices[g]):
+                    raise ValueError(f"slab {g}: expected {per} contiguous complex64 on cuda:{self.devices[g]}")
+        pin = (ctypes.c_void_p * self.ngpu)(*[t.data_ptr() for t in slabs_in])
+        pout = (ctypes.c_void_p * self.ngpu)(*[t.data_ptr() for t in slabs_out])
+        _check(_lib.fft_dplan_exec(self._h, pin, pout))
+        return slabs_out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.fft_dplan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
 def fft(x, direction: int = FFT_FORWARD, variant: int = VARIANT_AUTO, out=None):
     """One-shot batched FFT of a (B, N) complex64 CUDA tensor (plan per call)."""
     b, n = x.shape
@@ -194,10 +286,16 @@ class StreamOptions:
     chunks to record (``timeline_out``, shape (chunks, 8) float64 seconds)."""
 
     def __init__(self, n=0, chunk_bytes=0, depth=0, variant=VARIANT_AUTO, io_threads=0, direct_io=False,
-                 numa=True, taps=None, timeline=0, real=False):
+                 numa=True, taps=None, timeline=0, real=False, hop=0, window=None):
         import numpy as np
         self.c = _abi.StreamOpts()
         self.c.real = int(bool(real))
+        self.c.hop = int(hop)
+        self.window = None
+        if window is not None:
+            self.window = np.ascontiguousarray(np.asarray(window, dtype=np.float32))
+            self.c.window = self.window.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+            self.c.window_len = self.window.size
         self.c.chunk_bytes, self.c.depth, self.c.variant = int(chunk_bytes), int(depth), int(variant)
         self.c.io_threads, self.c.direct_io, self.c.numa = int(io_threads), int(bool(direct_io)), 0 if numa else -1
         self.tap_records = self.tap_out = self.timeline_out = None

@@ -26,9 +26,11 @@ VARIANT_AUTO, VARIANT_SINGLE, VARIANT_CLUSTER, VARIANT_FOURSTEP, VARIANT_IDENTIT
 VARIANT_NAMES = {0: "auto", 1: "single", 2: "cluster", 3: "fourstep", 4: "identity", 5: "pipe"}
 
 # Every symbol include/blockfft.h declares (checked by tests/test_abi.py).
-EXPORTED = ["fft_plan_create", "fft_plan_create_ex", "fft_plan_create_opts", "fft_plan_create_real", "fft_exec", "fft_exec_range",
+EXPORTED = ["fft_plan_create", "fft_plan_create_ex", "fft_plan_create_opts", "fft_plan_create_real",
+            "fft_plan_create_stft", "fft_exec", "fft_exec_range",
             "fft_plan_destroy", "fft_plan_get_info", "fft_file_records", "fft_partition",
             "fft_file", "fft_file_ex", "fft_file_range", "fft_exec_host", "fft_stream_host",
+            "fft_dplan_create", "fft_dplan_exec", "fft_dplan_geometry", "fft_dplan_destroy",
             "fft_numa_node", "fft_host_alloc", "fft_host_free", "fft_link_probe", "fft_stream_release", "fft_last_error", "fft_last_status", "fft_version"]
 
 
@@ -39,7 +41,7 @@ class PlanInfo(ctypes.Structure):
                 ("cluster", ctypes.c_int), ("scratch_bytes", ctypes.c_int64),
                 ("table_bytes", ctypes.c_int64), ("resident", ctypes.c_int),
                 ("exclusive", ctypes.c_int), ("ring_records", ctypes.c_int), ("ring_lag", ctypes.c_int),
-                ("real", ctypes.c_int)]
+                ("real", ctypes.c_int), ("hop", ctypes.c_int64)]
 
 
 class PlanOpts(ctypes.Structure):
@@ -53,7 +55,9 @@ class StreamOpts(ctypes.Structure):
                 ("direct_io", ctypes.c_int), ("numa", ctypes.c_int),
                 ("tap_records", ctypes.POINTER(ctypes.c_int64)), ("tap_count", ctypes.c_int64),
                 ("tap_out", ctypes.c_void_p), ("timeline", ctypes.POINTER(ctypes.c_double)),
-                ("timeline_chunks", ctypes.c_int64), ("real", ctypes.c_int)]
+                ("timeline_chunks", ctypes.c_int64), ("real", ctypes.c_int),
+                ("hop", ctypes.c_int64), ("window", ctypes.POINTER(ctypes.c_float)),
+                ("window_len", ctypes.c_int64)]
 
 
 TIMELINE_FIELDS = 8
@@ -88,6 +92,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "fft_plan_create_ex": (vp, [i64, i64, i32, i32]),
         "fft_plan_create_opts": (vp, [i64, i64, i32, ctypes.POINTER(PlanOpts)]),
         "fft_plan_create_real": (vp, [i64, i64, i32]),
+        "fft_plan_create_stft": (vp, [i64, i64, i64, i32, ctypes.POINTER(ctypes.c_float)]),
         "fft_exec": (i32, [vp, vp, vp, vp]),
         "fft_exec_range": (i32, [vp, vp, vp, i64, vp]),
         "fft_plan_destroy": (None, [vp]),
@@ -104,6 +109,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "fft_file_range": (i32, [ctypes.c_char_p, ctypes.c_char_p, i64, i32, i64, i64, i32,
                                  ctypes.POINTER(StreamOpts), ctypes.POINTER(StreamStats)]),
         "fft_numa_node": (i32, [i32]),
+        "fft_dplan_create": (vp, [i64, i32, ctypes.POINTER(i32), i32]),
+        "fft_dplan_exec": (i32, [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]),
+        "fft_dplan_geometry": (i32, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i32)]),
+        "fft_dplan_destroy": (None, [vp]),
         "fft_host_alloc": (vp, [i64, i32]),
         "fft_host_free": (None, [vp]),
         "fft_link_probe": (i32, [i32, vp, vp, i64, i32, ctypes.POINTER(ctypes.c_double)]),

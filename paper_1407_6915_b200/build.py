@@ -66,7 +66,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     # translation units compile concurrently (each holds its own kernel instantiations)
     stress_objs = []
     units = [(u, k, "") for u, k in (("plan.cu", "cu"), ("kern_rows.cu", "cu"), ("kern_cluster.cu", "cu"),
-                                     ("kern_pipe.cu", "cu"), ("kern_pipe3.cu", "cu"), ("real.cu", "cu"),
+                                     ("kern_pipe.cu", "cu"), ("kern_pipe3.cu", "cu"), ("real.cu", "cu"), ("dist.cu", "cu"),
                                      ("stream.cpp", "cpp"))]
     units += [(u, "cu", "stress") for u in STRESS_UNITS]
     for src, kind, flavour in units:

@@ -168,7 +168,10 @@ struct RowsMinBlocks {  // CTAs per SM the register budget is sized for
 template <int L, int B, bool INV, int PP = 16, int MINB = 0>   // MINB > 0 overrides the register budget
 __global__ void __launch_bounds__(B * Sched<L, PP>::T, MINB > 0 ? MINB : RowsMinBlocks<L, B, PP>::V)
 k_rows(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
-       const float2* __restrict__ tw, float scale) {
+       const float2* __restrict__ tw, float scale, int64_t istride, const float* __restrict__ window) {
+    // istride: elements between consecutive input records (L for records; the
+    // hop for STFT frames); window: optional real
+    // per-sample weights w[0..L) applied on load (STFT), nullptr = none
     using S = Sched<L, PP>;
     constexpr int P = S::P, T = S::T;
     extern __shared__ float2 sm[];
@@ -179,11 +182,15 @@ k_rows(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
     for (int64_t g = blockIdx.x; g * B < nrec; g += gridDim.x) {
         const int64_t r = g * B + b;
         const bool ok = r < nrec;
-        const float2* src = in + r * (int64_t)L + t;
+        const float2* src = in + r * istride + t;
         float2 v[P];
 #pragma unroll
         for (int s = 0; s < P; ++s) {
             float2 x = ok ? ld_stream(src + s * T) : make_float2(0.f, 0.f);
+            if (window) {
+                const float w = __ldg(window + t + s * T);
+                x = make_float2(x.x * w, x.y * w);
+            }
             v[s] = INV ? conjf2(x) : x;
         }
         fft_engine<L, PP>(v, t, sm, addr, tab);
@@ -276,6 +283,26 @@ k_fs_rows(const float2* __restrict__ y, float2* __restrict__ out, int64_t nrec, 
     }
 }
 
+
+// ======================================================================
+// STFT framing: frame f of a signal,
+// out[f][j] = w[j] * in[f * hop + j] (w = nullptr: rectangular), for frames
+// too long for the single-pass kernel (which frames and windows on load);
+// the batched transform then runs in place on `out`.
+// ======================================================================
+static __global__ void k_frames(const float2* __restrict__ in, float2* __restrict__ out, int64_t frames, int64_t n,
+                                int64_t hop, const float* __restrict__ window) {
+    const int64_t total = frames * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = i / n, j = i - f * n;
+        float2 x = __ldcs(in + f * hop + j);
+        if (window) {
+            const float w = __ldg(window + j);
+            x = make_float2(x.x * w, x.y * w);
+        }
+        __stcs(out + i, x);
+    }
+}
 
 // ======================================================================
 // Identity kernel: out = in, bit-exact, 16-byte vectors.

@@ -164,7 +164,9 @@ struct fft_plan {
     int grid_a = 0, grid_b = 0;       // persistent/capped grid sizes (per full batch)
     int occ_a = 0, occ_b = 0;
     int real = 0;                     // 1: real records (fft_plan_create_real), n reals each
-    fft_plan* inner = nullptr;        // real: the n/2-point complex plan
+    int64_t hop = 0;                  // > 0: STFT frames every `hop` samples (fft_plan_create_stft)
+    float* d_win = nullptr;           // STFT: optional window, n floats
+    fft_plan* inner = nullptr;        // real: the n/2-point complex plan; STFT: the frames' plan
     int rt_lb = 0;                    // real: two-level W_n split (tw_a = hi, tw_b = lo)
 };
 
@@ -378,6 +380,7 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, const fft_p
 static void plan_free(fft_plan* p) {
     if (!p) return;
     if (p->inner) plan_free(p->inner);
+    if (p->d_win) cudaFree(p->d_win);
     if (p->d_tab) cudaFree(p->d_tab);
     if (p->d_scratch) cudaFree(p->d_scratch);
     if (p->d_ctr) cudaFree(p->d_ctr);
@@ -486,6 +489,47 @@ extern "C" fft_plan* fft_plan_create_real(int64_t n, int64_t batch, int dir) {
     return p;
 }
 
+extern "C" fft_plan* fft_plan_create_stft(int64_t n, int64_t hop, int64_t frames, int dir, const float* window) {
+    bfft_clear_error();
+    if (validate(n, frames, dir)) return nullptr;
+    if (hop < 1) {
+        bfft_set_error(FFT_E_ARG, "hop must be >= 1: %lld", (long long)hop);
+        return nullptr;
+    }
+    fft_plan* p = new (std::nothrow) fft_plan();
+    if (!p) {
+        bfft_set_error(FFT_E_NOMEM, "out of host memory");
+        return nullptr;
+    }
+    auto fail = [&]() -> fft_plan* {
+        std::string keep = g_err;
+        int code = g_code;
+        plan_free(p);
+        g_err = keep;
+        g_code = code;
+        return nullptr;
+    };
+    p->n = n;
+    p->batch = frames;
+    p->dir = dir;
+    p->hop = hop;
+    p->log2n = ilog2((int)n);
+    p->inner = fft_plan_create_opts(n, frames, dir, nullptr);
+    if (!p->inner) return fail();
+    p->device = p->inner->device;
+    p->sms = p->inner->sms;
+    p->variant = p->inner->variant;
+    if (window) {
+        cudaError_t e = cudaMalloc(&p->d_win, sizeof(float) * n);
+        if (e == cudaSuccess) e = cudaMemcpy(p->d_win, window, sizeof(float) * n, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            bfft_set_error(FFT_E_CUDA, "window upload failed: %s", cudaGetErrorString(e));
+            return fail();
+        }
+    }
+    return p;
+}
+
 extern "C" void fft_plan_destroy(fft_plan* p) { plan_free(p); }
 
 extern "C" int fft_plan_get_info(const fft_plan* p, fft_plan_info* info) {
@@ -497,9 +541,17 @@ extern "C" int fft_plan_get_info(const fft_plan* p, fft_plan_info* info) {
         info->kernels_per_exec += 1;                 // + the split / merge kernel
         info->table_bytes += (int64_t)p->tab_bytes;
         info->real = 1;
+        info->hop = 0;
         return rc;
     }
     info->real = 0;
+    if (p->hop) {
+        int rc = fft_plan_get_info(p->inner, info);
+        info->hop = p->hop;
+        if (p->inner->variant != FFT_VARIANT_SINGLE) info->kernels_per_exec += 1;   // + the framing kernel
+        return rc;
+    }
+    info->hop = 0;
     info->n = p->n;
     info->batch = p->batch;
     info->dir = p->dir;
@@ -522,8 +574,10 @@ extern "C" int fft_plan_get_info(const fft_plan* p, fft_plan_info* info) {
 }
 
 // ------------------------------------------------------------ exec
-static int launch(const fft_plan* p, const float2* in, float2* out, int64_t count, cudaStream_t st) {
+static int launch(const fft_plan* p, const float2* in, float2* out, int64_t count, cudaStream_t st,
+                  int64_t istride = 0, const float* window = nullptr) {
     const int64_t n = p->n;
+    if (istride == 0) istride = n;
     switch (p->variant) {
         case FFT_VARIANT_IDENTITY: {
             const int64_t n16 = count * n * 8 / 16;
@@ -537,7 +591,7 @@ static int launch(const fft_plan* p, const float2* in, float2* out, int64_t coun
             const int64_t groups = (count + p->ka.cols - 1) / p->ka.cols;
             const int grid = (int)std::min<int64_t>(groups, (int64_t)p->sms * p->occ_a * 8);
             auto fn = (RowFn)p->ka.fn;
-            fn<<<grid, p->ka.threads, p->ka.smem, st>>>(in, out, count, p->tw_a, p->scale);
+            fn<<<grid, p->ka.threads, p->ka.smem, st>>>(in, out, count, p->tw_a, p->scale, istride, window);
             break;
         }
         case FFT_VARIANT_CLUSTER: {
@@ -613,12 +667,31 @@ extern "C" int fft_exec_range(const fft_plan* p, const void* in, void* out, int6
         return bfft_set_error(FFT_E_ARG, "record count out of range: expected 1..%lld, got %lld", (long long)p->batch, (long long)count);
     const uintptr_t bytes = (uintptr_t)(count * p->n * (p->real ? 4 : 8));
     const uintptr_t a = (uintptr_t)in, b = (uintptr_t)out;
-    if (a != b && a < b + bytes && b < a + bytes)
+    if (p->hop) {
+        // STFT: frames overlap in the input, so input and output must be disjoint
+        const uintptr_t in_bytes = (uintptr_t)(((count - 1) * p->hop + p->n) * 8);
+        if (a < b + bytes && b < a + in_bytes)
+            return bfft_set_error(FFT_E_ARG, "STFT input and output overlap");
+    } else if (a != b && a < b + bytes && b < a + bytes) {
         return bfft_set_error(FFT_E_ARG, "input and output partially overlap");
+    }
     int dev = -1;
     CUDA_TRY(cudaGetDevice(&dev));
     if (dev != p->device)
         return bfft_set_error(FFT_E_DEVICE, "plan belongs to device %d, current device is %d", p->device, dev);
+    if (p->hop) {
+        // STFT frames: the single-pass kernel frames and windows on load; longer
+        // frames are framed into `out` first and transformed in place
+        cudaStream_t st = (cudaStream_t)stream;
+        if (p->inner->variant == FFT_VARIANT_SINGLE)
+            return launch(p->inner, (const float2*)in, (float2*)out, count, st, p->hop, p->d_win);
+        const int threads = 256;
+        const int grid = (int)std::min<int64_t>((count * p->n + threads - 1) / threads, (int64_t)p->sms * 16);
+        k_frames<<<grid, threads, 0, st>>>((const float2*)in, (float2*)out, count, p->n, p->hop, p->d_win);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return bfft_set_error(FFT_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+        return launch(p->inner, (const float2*)out, (float2*)out, count, st);
+    }
     if (p->real) {
         // real records: forward = complex n/2 transform, then the split in place;
         // inverse = the merge into `out`, then the complex inverse in place

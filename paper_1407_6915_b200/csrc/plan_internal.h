@@ -26,7 +26,7 @@ struct ClusterChoice {
 };
 
 // kernel signatures, by family (launch casts KernelSet::fn to these)
-using RowFn = void (*)(const float2*, float2*, int64_t, const float2*, float);
+using RowFn = void (*)(const float2*, float2*, int64_t, const float2*, float, int64_t, const float*);
 using ColFn = void (*)(const float2*, float2*, int64_t, int, const float2*);
 using RowTFn = void (*)(const float2*, float2*, int64_t, int, const float2*, float);
 using ClusterFn = void (*)(const CUtensorMap, float2*, int64_t, const float2*, const float2*, float);

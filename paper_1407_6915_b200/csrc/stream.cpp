@@ -125,18 +125,20 @@ struct Span {
     int64_t bytes;
 };
 
-// A source yields records [first, first+count) of the logical stream.  A
-// pinned source exposes them directly (up to two spans: rings wrap), else
-// the reader copies them into a pinned slot with read().
+// A source yields the bytes [off, off+len) of the logical input stream; a
+// sink consumes bytes at their offsets of the output.  Pinned memory sources
+// and sinks expose the bytes directly (up to two spans: rings wrap), else the
+// reader / writer copy through a pinned slot.  Offsets are bytes so a chunk of
+// STFT frames can read its halo (the N - hop samples it shares with the next).
 struct Source {
     virtual ~Source() = default;
-    virtual int direct(int64_t first, int64_t count, Span out[2]) { (void)first; (void)count; (void)out; return 0; }
-    virtual int read(int64_t first, int64_t count, void* dst) = 0;
+    virtual int direct(int64_t off, int64_t len, Span out[2]) { (void)off; (void)len; (void)out; return 0; }
+    virtual int read(int64_t off, int64_t len, void* dst) = 0;
 };
 struct Sink {
     virtual ~Sink() = default;
-    virtual int direct(int64_t first, int64_t count, Span out[2]) { (void)first; (void)count; (void)out; return 0; }
-    virtual int write(int64_t first, int64_t count, const void* src) = 0;
+    virtual int direct(int64_t off, int64_t len, Span out[2]) { (void)off; (void)len; (void)out; return 0; }
+    virtual int write(int64_t off, int64_t len, const void* src) = 0;
 };
 
 int io_err(const char* what, const char* path, int64_t off, int64_t want, int64_t got, int err) {
@@ -199,20 +201,19 @@ int parallel_io(int64_t len, int nt, F&& piece) {
     return 0;
 }
 
-// File source: record r at byte r*rb; bytes past EOF read as zero (the final
-// record is zero-padded, reading c6).  With O_DIRECT the
-// read of the last partial block is rounded up to 4 KiB (the pinned slot has
-// room: slots are whole records and rb is a 4 KiB multiple then).
+// File source: bytes past EOF read as zero (the final record or frame is
+// zero-padded, reading c6).  With O_DIRECT the read of the
+// last partial block is rounded up to 4 KiB (the pinned slot has room: slots
+// are whole 4 KiB-multiple records then).
 struct FileSource : Source {
     int fd;
-    int64_t size, rb;
+    int64_t size;
     const char* path;
     int nt;
     bool odirect;
-    FileSource(int f, int64_t s, int64_t recbytes, const char* p, int threads, bool od)
-        : fd(f), size(s), rb(recbytes), path(p), nt(threads), odirect(od) {}
-    int read(int64_t first, int64_t count, void* dst) override {
-        const int64_t off = first * rb, len = count * rb;
+    FileSource(int f, int64_t s, const char* p, int threads, bool od)
+        : fd(f), size(s), path(p), nt(threads), odirect(od) {}
+    int read(int64_t off, int64_t len, void* dst) override {
         const int64_t avail = std::max<int64_t>(0, std::min<int64_t>(len, size - off));
         if (avail > 0) {
             const int64_t want = odirect ? std::min<int64_t>(len, (avail + 4095) & ~4095ll) : avail;
@@ -241,14 +242,12 @@ struct FileSource : Source {
 };
 struct FileSink : Sink {
     int fd;
-    int64_t rb;
     const char* path;
     int nt;
-    FileSink(int f, int64_t recbytes, const char* p, int threads) : fd(f), rb(recbytes), path(p), nt(threads) {}
-    int write(int64_t first, int64_t count, const void* src) override {
-        const int64_t off = first * rb;
+    FileSink(int f, const char* p, int threads) : fd(f), path(p), nt(threads) {}
+    int write(int64_t off, int64_t len, const void* src) override {
         std::atomic<int> err{0};
-        int r = parallel_io(count * rb, nt, [&](int64_t a, int64_t n) {
+        int r = parallel_io(len, nt, [&](int64_t a, int64_t n) {
             if (pwrite_full(fd, (const char*)src + a, n, off + a) != 0) {
                 err = errno;
                 return 1;
@@ -262,26 +261,26 @@ struct FileSink : Sink {
     }
 };
 // Host-memory ring source / sink (fft_stream_host, fft_exec_host): logical
-// record r lives at ring record r mod cap.  Pinned memory is copied directly.
-int ring_spans(char* base, int64_t cap, int64_t rb, int64_t first, int64_t count, Span out[2]) {
-    const int64_t s = first % cap, n1 = std::min<int64_t>(count, cap - s);
-    out[0] = Span{base + s * rb, n1 * rb};
-    if (n1 == count) return 1;
-    out[1] = Span{base, (count - n1) * rb};
+// byte b lives at ring byte b mod cap (cap = ring records x record bytes).
+// Pinned memory is copied directly.
+int ring_spans(char* base, int64_t cap, int64_t off, int64_t len, Span out[2]) {
+    const int64_t s = off % cap, n1 = std::min<int64_t>(len, cap - s);
+    out[0] = Span{base + s, n1};
+    if (n1 == len) return 1;
+    out[1] = Span{base, len - n1};
     return 2;
 }
 struct MemSource : Source {
     char* base;
-    int64_t cap, rb;
+    int64_t cap;
     bool pinned;
-    MemSource(const void* b, int64_t c, int64_t recbytes, bool pin)
-        : base((char*)b), cap(c), rb(recbytes), pinned(pin) {}
-    int direct(int64_t first, int64_t count, Span out[2]) override {
-        return pinned ? ring_spans(base, cap, rb, first, count, out) : 0;
+    MemSource(const void* b, int64_t c, bool pin) : base((char*)b), cap(c), pinned(pin) {}
+    int direct(int64_t off, int64_t len, Span out[2]) override {
+        return pinned ? ring_spans(base, cap, off, len, out) : 0;
     }
-    int read(int64_t first, int64_t count, void* dst) override {
+    int read(int64_t off, int64_t len, void* dst) override {
         Span sp[2];
-        const int ns = ring_spans(base, cap, rb, first, count, sp);
+        const int ns = ring_spans(base, cap, off, len, sp);
         char* d = (char*)dst;
         for (int i = 0; i < ns; ++i) {
             memcpy(d, sp[i].p, (size_t)sp[i].bytes);
@@ -292,15 +291,15 @@ struct MemSource : Source {
 };
 struct MemSink : Sink {
     char* base;
-    int64_t cap, rb;
+    int64_t cap;
     bool pinned;
-    MemSink(void* b, int64_t c, int64_t recbytes, bool pin) : base((char*)b), cap(c), rb(recbytes), pinned(pin) {}
-    int direct(int64_t first, int64_t count, Span out[2]) override {
-        return pinned ? ring_spans(base, cap, rb, first, count, out) : 0;
+    MemSink(void* b, int64_t c, bool pin) : base((char*)b), cap(c), pinned(pin) {}
+    int direct(int64_t off, int64_t len, Span out[2]) override {
+        return pinned ? ring_spans(base, cap, off, len, out) : 0;
     }
-    int write(int64_t first, int64_t count, const void* src) override {
+    int write(int64_t off, int64_t len, const void* src) override {
         Span sp[2];
-        const int ns = ring_spans(base, cap, rb, first, count, sp);
+        const int ns = ring_spans(base, cap, off, len, sp);
         const char* s = (const char*)src;
         for (int i = 0; i < ns; ++i) {
             memcpy(sp[i].p, s, (size_t)sp[i].bytes);
@@ -352,6 +351,8 @@ struct Opts {
     double* timeline = nullptr;
     int64_t timeline_chunks = 0;
     int real = 0;
+    int64_t hop = 0;              // > 0: STFT frames every hop samples (fft_plan_create_stft)
+    std::vector<float> window;    // STFT window (empty = rectangular)
 };
 
 // Runtime options of the streamer: the chunk size is the paper's one tunable
@@ -372,6 +373,8 @@ Opts resolve(const fft_stream_opts* o) {
         r.timeline = o->timeline;
         r.timeline_chunks = o->timeline ? o->timeline_chunks : 0;
         r.real = o->real != 0;
+        r.hop = o->hop;
+        if (o->hop > 0 && o->window) r.window.assign(o->window, o->window + o->window_len);
     }
     return r;
 }
@@ -379,12 +382,30 @@ Opts resolve(const fft_stream_opts* o) {
 // bytes per record: n complex64 (8n), or n float32 / n/2 packed complex64 (4n)
 int64_t rec_bytes(int64_t n, const Opts& o) { return o.real ? 4 * n : 8 * n; }
 
+// Byte geometry of the logical input and output streams, per record (or STFT
+// frame) f: input bytes [f*in_rb, f*in_rb + in_rb + in_extra) — in_extra > 0
+// is the halo an STFT frame shares with the next — output [f*out_rb, +out_rb).
+struct Geom {
+    int64_t in_rb, in_extra, out_rb;
+    int64_t in_off(int64_t f) const { return f * in_rb; }
+    int64_t in_len(int64_t cnt) const { return cnt * in_rb + in_extra; }
+};
+Geom geom_of(int64_t n, const Opts& o) {
+    if (o.hop > 0) return Geom{8 * o.hop, 8 * (n - o.hop), 8 * n};
+    return Geom{rec_bytes(n, o), 0, rec_bytes(n, o)};
+}
+
 int check_opts(const fft_stream_opts* o) {
     if (!o) return FFT_OK;
     if (o->chunk_bytes < 0 || o->depth < 0 || o->io_threads < 0 || o->tap_count < 0 || o->timeline_chunks < 0)
         return bfft_set_error(FFT_E_ARG, "invalid stream options: chunk_bytes=%lld depth=%d io_threads=%d "
                               "tap_count=%lld timeline_chunks=%lld", (long long)o->chunk_bytes, o->depth,
                               o->io_threads, (long long)o->tap_count, (long long)o->timeline_chunks);
+    if (o->hop < 0 || (o->hop > 0 && o->real))
+        return bfft_set_error(FFT_E_ARG, "invalid stream options: hop=%lld real=%d (STFT frames are complex)",
+                              (long long)o->hop, o->real);
+    if (o->hop > 0 && o->window && o->window_len <= 0)
+        return bfft_set_error(FFT_E_ARG, "window_len must be the frame length: %lld", (long long)o->window_len);
     if (o->tap_count > 0 && (!o->tap_records || !o->tap_out))
         return bfft_set_error(FFT_E_ARG, "tap_count %lld needs tap_records and tap_out", (long long)o->tap_count);
     for (int64_t i = 1; i < o->tap_count; ++i)
@@ -400,13 +421,14 @@ int check_opts(const fft_stream_opts* o) {
 // frees every idle context.
 struct StreamCtx {
     int device = 0, dir = 0, variant = 0, depth = 0, node = -1, real = 0;
-    int64_t n = 0, crec = 0;
+    int64_t n = 0, crec = 0, hop = 0;
+    std::vector<float> window;
     bool stage_in = false, stage_out = false, busy = false;
     fft_plan* plan = nullptr;
     cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
     cudaEvent_t base = nullptr;
     std::vector<cudaEvent_t> e0, e1, e2, e3;
-    std::vector<void*> dbuf, hin, hout;
+    std::vector<void*> dbuf, dout, hin, hout;   // dout: STFT output slots (records: in place in dbuf)
     void release() {
         int cur = 0;
         cudaGetDevice(&cur);
@@ -418,8 +440,9 @@ struct StreamCtx {
             for (auto ev : *v)
                 if (ev) cudaEventDestroy(ev);
         if (base) cudaEventDestroy(base);
-        for (void* b : dbuf)
-            if (b) cudaFree(b);
+        for (auto* v : {&dbuf, &dout})
+            for (void* b : *v)
+                if (b) cudaFree(b);
         for (auto* v : {&hin, &hout})
             for (void* b : *v)
                 if (b) cudaFreeHost(b);
@@ -448,14 +471,14 @@ int ctx_fail(StreamCtx* c, StreamCtx** out, int rc) {
                                                    cudaGetErrorString(e_)));                        \
     } while (0)
 
-int acquire_ctx(int device, int64_t n, int dir, int variant, int real, int64_t crec, int D, bool stage_in,
+int acquire_ctx(int device, int64_t n, int dir, const Opts& o, const Geom& g, int64_t crec, int D, bool stage_in,
                 bool stage_out, int node, StreamCtx** out) {
     {
-        std::lock_guard<std::mutex> g(g_ctx_mu);
+        std::lock_guard<std::mutex> lk(g_ctx_mu);
         for (StreamCtx* c : g_ctx)
-            if (!c->busy && c->device == device && c->n == n && c->dir == dir && c->variant == variant &&
+            if (!c->busy && c->device == device && c->n == n && c->dir == dir && c->variant == o.variant &&
                 c->crec == crec && c->depth == D && c->stage_in == stage_in && c->stage_out == stage_out &&
-                c->node == node && c->real == real) {
+                c->node == node && c->real == o.real && c->hop == o.hop && c->window == o.window) {
                 c->busy = true;
                 *out = c;
                 return FFT_OK;
@@ -466,17 +489,23 @@ int acquire_ctx(int device, int64_t n, int dir, int variant, int real, int64_t c
     c->device = device;
     c->n = n;
     c->dir = dir;
-    c->variant = variant;
+    c->variant = o.variant;
     c->crec = crec;
     c->depth = D;
     c->stage_in = stage_in;
     c->stage_out = stage_out;
     c->node = node;
-    c->real = real;
+    c->real = o.real;
+    c->hop = o.hop;
+    c->window = o.window;
     c->busy = true;
     CKC(cudaSetDevice(device));
-    c->plan = real ? fft_plan_create_real(n, crec, dir)
-                   : fft_plan_create_ex(n, crec, dir, dir == 0 ? FFT_VARIANT_IDENTITY : variant);
+    if (o.hop > 0)
+        c->plan = fft_plan_create_stft(n, o.hop, crec, dir, o.window.empty() ? nullptr : o.window.data());
+    else if (o.real)
+        c->plan = fft_plan_create_real(n, crec, dir);
+    else
+        c->plan = fft_plan_create_ex(n, crec, dir, dir == 0 ? FFT_VARIANT_IDENTITY : o.variant);
     if (!c->plan) {
         const int code = bfft_last_code();
         delete c;
@@ -492,24 +521,26 @@ int acquire_ctx(int device, int64_t n, int dir, int variant, int real, int64_t c
         for (int i = 0; i < D; ++i) CKC(cudaEventCreate(&(*v)[i]));
     }
     c->dbuf.assign(D, nullptr);
+    c->dout.assign(D, nullptr);
     c->hin.assign(D, nullptr);
     c->hout.assign(D, nullptr);
-    const size_t bytes = (size_t)(crec * (real ? 4 : 8) * n);
+    const size_t in_bytes = (size_t)g.in_len(crec), out_bytes = (size_t)(crec * g.out_rb);
+    const bool separate = o.hop > 0;   // STFT: output slot apart from the (overlapping) input
     NumaScope numa(node);   // pinned slots on the GPU's NUMA node (first touch happens in cudaHostAlloc)
     for (int i = 0; i < D; ++i) {
-        cudaError_t e = cudaMalloc(&c->dbuf[i], bytes);
+        const size_t dbytes = separate ? in_bytes : std::max(in_bytes, out_bytes);
+        cudaError_t e = cudaMalloc(&c->dbuf[i], dbytes);
+        if (e == cudaSuccess && separate) e = cudaMalloc(&c->dout[i], out_bytes);
         if (e != cudaSuccess)
-            return ctx_fail(c, out, bfft_set_error(FFT_E_NOMEM, "cudaMalloc(%zu) for stream slot failed: %s", bytes,
+            return ctx_fail(c, out, bfft_set_error(FFT_E_NOMEM, "cudaMalloc(%zu) for stream slot failed: %s", dbytes,
                                                    cudaGetErrorString(e)));
-        for (auto* v : {&c->hin, &c->hout}) {
-            if ((v == &c->hin && !stage_in) || (v == &c->hout && !stage_out)) continue;
-            e = cudaHostAlloc(&(*v)[i], bytes, cudaHostAllocPortable);
-            if (e != cudaSuccess)
-                return ctx_fail(c, out, bfft_set_error(FFT_E_NOMEM, "cudaHostAlloc(%zu) for stream slot failed: %s",
-                                                       bytes, cudaGetErrorString(e)));
-        }
+        if (stage_in) e = cudaHostAlloc(&c->hin[i], in_bytes, cudaHostAllocPortable);
+        if (e == cudaSuccess && stage_out) e = cudaHostAlloc(&c->hout[i], out_bytes, cudaHostAllocPortable);
+        if (e != cudaSuccess)
+            return ctx_fail(c, out, bfft_set_error(FFT_E_NOMEM, "cudaHostAlloc for stream slot failed: %s",
+                                                   cudaGetErrorString(e)));
     }
-    std::lock_guard<std::mutex> g(g_ctx_mu);
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
     g_ctx.push_back(c);
     return FFT_OK;
 }
@@ -561,16 +592,17 @@ struct Progress {
 // The per-GPU pipeline over logical records [first, first+count).
 int run_pipeline(int device, int64_t n, int dir, int64_t first, int64_t count, Source* src, Sink* dst,
                  const Opts& o, fft_stream_stats* st) {
-    const int64_t rb = rec_bytes(n, o);
-    const int64_t crec = std::max<int64_t>(1, std::min<int64_t>(count, o.chunk_bytes / rb));
+    const Geom g = geom_of(n, o);
+    const int64_t rb = g.out_rb;
+    const int64_t crec = std::max<int64_t>(1, std::min<int64_t>(count, o.chunk_bytes / std::max(g.in_rb, g.out_rb)));
     const int D = o.depth;
     Span probe[2];
-    const bool stage_in = src->direct(first, 1, probe) == 0;
-    const bool stage_out = dst->direct(first, 1, probe) == 0;
+    const bool stage_in = src->direct(g.in_off(first), g.in_len(1), probe) == 0;
+    const bool stage_out = dst->direct(first * rb, rb, probe) == 0;
     const int node = o.numa < 0 ? -1 : gpu_numa_node(device);
     st->numa_node = node;
     StreamCtx* c = nullptr;
-    int rc = acquire_ctx(device, n, dir, o.variant, o.real, crec, D, stage_in, stage_out, node, &c);
+    int rc = acquire_ctx(device, n, dir, o, g, crec, D, stage_in, stage_out, node, &c);
     if (rc) return rc;
     const int64_t nchunks = (count + crec - 1) / crec;
     auto chunk_first = [&](int64_t k) { return first + k * crec; };
@@ -611,7 +643,7 @@ int run_pipeline(int device, int64_t n, int dir, int64_t first, int64_t count, S
                     }
                 }
                 const double a = now_s();
-                const int r = src->read(chunk_first(k), chunk_count(k), c->hin[i]);
+                const int r = src->read(g.in_off(chunk_first(k)), g.in_len(chunk_count(k)), c->hin[i]);
                 const double b = now_s();
                 read_s += b - a;
                 tl_set(k, 0, a - t0);
@@ -660,7 +692,7 @@ int run_pipeline(int device, int64_t n, int dir, int64_t first, int64_t count, S
             Span sp[2];
             if (stage_out) {
                 const double t_a = now_s();
-                const int r = dst->write(f, cnt, c->hout[i]);
+                const int r = dst->write(f * rb, cnt * rb, c->hout[i]);
                 const double t_b = now_s();
                 write_s += t_b - t_a;
                 tl_set(k, 6, t_a - t0);
@@ -671,7 +703,7 @@ int run_pipeline(int device, int64_t n, int dir, int64_t first, int64_t count, S
                 }
                 outp = (const char*)c->hout[i];
             } else {
-                dst->direct(f, cnt, sp);
+                dst->direct(f * rb, cnt * rb, sp);
                 tl_set(k, 6, now_s() - t0);
                 tl_set(k, 7, now_s() - t0);
             }
@@ -698,6 +730,8 @@ int run_pipeline(int device, int64_t n, int dir, int64_t first, int64_t count, S
         // slot i free (its previous chunk retired by the writer), input loaded
         if (!pg.wait([&] { return pg.written > k - D && (!stage_in || pg.loaded > k); })) break;
         char* dptr = (char*)c->dbuf[i];
+        char* optr = c->dout[i] ? (char*)c->dout[i] : dptr;   // STFT: separate output slot
+        const int64_t in_len = g.in_len(cnt);
         Span sp[2];
         auto fail_cuda = [&](const char* what, cudaError_t e) {
             pg.fail(bfft_set_error(FFT_E_CUDA, "%s failed: %s", what, cudaGetErrorString(e)));
@@ -714,9 +748,9 @@ int run_pipeline(int device, int64_t n, int dir, int64_t first, int64_t count, S
         CKL(cudaStreamWaitEvent(c->sh, c->e3[i], 0));   // device slot's previous D2H done
         CKL(cudaEventRecord(c->e0[i], c->sh));
         if (stage_in) {
-            CKL(cudaMemcpyAsync(dptr, c->hin[i], (size_t)(cnt * rb), cudaMemcpyHostToDevice, c->sh));
+            CKL(cudaMemcpyAsync(dptr, c->hin[i], (size_t)in_len, cudaMemcpyHostToDevice, c->sh));
         } else {
-            const int ns = src->direct(f, cnt, sp);
+            const int ns = src->direct(g.in_off(f), in_len, sp);
             int64_t off = 0;
             for (int s = 0; s < ns; ++s) {
                 if ((ce = cudaMemcpyAsync(dptr + off, sp[s].p, (size_t)sp[s].bytes, cudaMemcpyHostToDevice, c->sh)) !=
@@ -731,7 +765,7 @@ int run_pipeline(int device, int64_t n, int dir, int64_t first, int64_t count, S
         }
         CKL(cudaEventRecord(c->e1[i], c->sh));
         CKL(cudaStreamWaitEvent(c->sc, c->e1[i], 0));
-        rc = fft_exec_range(c->plan, dptr, dptr, cnt, c->sc);
+        rc = fft_exec_range(c->plan, dptr, optr, cnt, c->sc);
         if (rc) {
             pg.fail(rc);
             break;
@@ -739,12 +773,12 @@ int run_pipeline(int device, int64_t n, int dir, int64_t first, int64_t count, S
         CKL(cudaEventRecord(c->e2[i], c->sc));
         CKL(cudaStreamWaitEvent(c->sd, c->e2[i], 0));
         if (stage_out) {
-            CKL(cudaMemcpyAsync(c->hout[i], dptr, (size_t)(cnt * rb), cudaMemcpyDeviceToHost, c->sd));
+            CKL(cudaMemcpyAsync(c->hout[i], optr, (size_t)(cnt * rb), cudaMemcpyDeviceToHost, c->sd));
         } else {
-            const int ns = dst->direct(f, cnt, sp);
+            const int ns = dst->direct(f * rb, cnt * rb, sp);
             int64_t off = 0;
             for (int s = 0; s < ns; ++s) {
-                if ((ce = cudaMemcpyAsync(sp[s].p, dptr + off, (size_t)sp[s].bytes, cudaMemcpyDeviceToHost, c->sd)) !=
+                if ((ce = cudaMemcpyAsync(sp[s].p, optr + off, (size_t)sp[s].bytes, cudaMemcpyDeviceToHost, c->sd)) !=
                     cudaSuccess)
                     break;
                 off += sp[s].bytes;
@@ -758,7 +792,7 @@ int run_pipeline(int device, int64_t n, int dir, int64_t first, int64_t count, S
 #undef CKL
         st->records += cnt;
         st->chunks += 1;
-        st->bytes_in += cnt * rb;
+        st->bytes_in += in_len;
         pg.set(pg.submitted, k + 1);
     }
     if (reader.joinable()) reader.join();
@@ -791,8 +825,17 @@ int check_n_dir(int64_t n, int dir, bool real) {
     return FFT_OK;
 }
 
-// records of a file: ceil(size / record bytes), the final one zero-padded (reading c6)
+// records (or STFT frames) of a file: ceil(size / record bytes), the final
+// one zero-padded (reading c6); STFT over L = size/8 samples:
+// F = 1 + ceil((L - n) / hop) frames (L <= n: one zero-padded frame)
 int64_t file_records_of(int64_t size, int64_t n, const Opts& o) {
+    if (o.hop > 0) {
+        if (size % 8)
+            return -bfft_set_error(FFT_E_ARG, "file size %lld is not a multiple of 8 bytes", (long long)size);
+        if (size == 0) return -bfft_set_error(FFT_E_EMPTY, "empty input");
+        const int64_t L = size / 8;
+        return L <= n ? 1 : 1 + (L - n + o.hop - 1) / o.hop;
+    }
     if (!o.real) return fft_file_records(size, n);
     if (size % 4)
         return -bfft_set_error(FFT_E_ARG, "file size %lld is not a multiple of 4 bytes", (long long)size);
@@ -812,7 +855,10 @@ int check_device(int device) {
 }
 
 // O_DIRECT needs 4 KiB-aligned offsets and lengths: records of 8N bytes with N >= 512.
-bool direct_ok(const Opts& o, int64_t n) { return o.direct_io && rec_bytes(n, o) % 4096 == 0; }
+bool direct_ok(const Opts& o, int64_t n) {
+    const Geom g = geom_of(n, o);
+    return o.direct_io && g.in_rb % 4096 == 0 && g.in_extra % 4096 == 0 && g.out_rb % 4096 == 0;
+}
 
 int open_input(const char* path, bool od, int* fd, int* fd_direct, int64_t* size) {
     *fd = open(path, O_RDONLY);
@@ -843,9 +889,11 @@ extern "C" int fft_stream_host(int64_t n, int64_t total_records, int dir, const 
         return bfft_set_error(FFT_E_ARG, "ring sizes must be >= 1: in_records=%lld out_records=%lld",
                               (long long)in_records, (long long)out_records);
     if ((rc = check_opts(opts)) || (rc = check_device(device))) return rc;
+    if (opts && opts->hop > 0)
+        return bfft_set_error(FFT_E_ARG, "STFT streaming (hop > 0) takes files (fft_file_ex / fft_file_range)");
     const Opts o = resolve(opts);
-    MemSource src(host_in, in_records, rec_bytes(n, o), is_pinned(host_in));
-    MemSink dst(host_out, out_records, rec_bytes(n, o), is_pinned(host_out));
+    MemSource src(host_in, in_records * rec_bytes(n, o), is_pinned(host_in));
+    MemSink dst(host_out, out_records * rec_bytes(n, o), is_pinned(host_out));
     fft_stream_stats st{};
     st.numa_node = -1;
     const double t0 = now_s();
@@ -880,7 +928,7 @@ extern "C" int fft_file_ex(const char* in_path, const char* out_path, int64_t n,
     int64_t size = 0;
     if ((rc = open_input(in_path, od, &fd, &fdd, &size))) return rc;
     const int64_t R = file_records_of(size, n, o);
-    const int64_t rb = rec_bytes(n, o);
+    const int64_t rb = geom_of(n, o).out_rb;
     if (R < 0) {
         close(fd);
         if (fdd >= 0) close(fdd);
@@ -910,8 +958,8 @@ extern "C" int fft_file_ex(const char* in_path, const char* out_path, int64_t n,
                 int64_t first = 0, count = 0;
                 fft_partition(R, ngpu, g, &first, &count);
                 if (count == 0) return;
-                FileSource src(fdd >= 0 ? fdd : fd, size, rb, in_path, o.io_threads, fdd >= 0);
-                FileSink dst(ofdd >= 0 ? ofdd : ofd, rb, tmp.c_str(), o.io_threads);
+                FileSource src(fdd >= 0 ? fdd : fd, size, in_path, o.io_threads, fdd >= 0);
+                FileSink dst(ofdd >= 0 ? ofdd : ofd, tmp.c_str(), o.io_threads);
                 fft_stream_stats st{};
                 st.direct_io = fdd >= 0 && ofdd >= 0;
                 rcs[g] = run_pipeline(g, n, dir, first, count, &src, &dst, o, &st);
@@ -954,7 +1002,6 @@ extern "C" int fft_file_range(const char* in_path, const char* out_path, int64_t
     int64_t size = 0;
     if ((rc = open_input(in_path, od, &fd, &fdd, &size))) return rc;
     const int64_t R = file_records_of(size, n, o);
-    const int64_t rb = rec_bytes(n, o);
     auto done = [&](int code) {
         close(fd);
         if (fdd >= 0) close(fdd);
@@ -978,8 +1025,8 @@ extern "C" int fft_file_range(const char* in_path, const char* out_path, int64_t
     const int ofd = open(out_path, O_WRONLY | O_CREAT, 0644);
     if (ofd < 0) return done(bfft_set_error(FFT_E_IO, "cannot open %s: %s", out_path, strerror(errno)));
     const int ofdd = od ? open(out_path, O_WRONLY | O_DIRECT) : -1;
-    FileSource src(fdd >= 0 ? fdd : fd, size, rb, in_path, o.io_threads, fdd >= 0);
-    FileSink dst(ofdd >= 0 ? ofdd : ofd, rb, out_path, o.io_threads);
+    FileSource src(fdd >= 0 ? fdd : fd, size, in_path, o.io_threads, fdd >= 0);
+    FileSink dst(ofdd >= 0 ? ofdd : ofd, out_path, o.io_threads);
     st.direct_io = fdd >= 0 && ofdd >= 0;
     const double t0 = now_s();
     rc = run_pipeline(device, n, dir, first_record, count, &src, &dst, o, &st);
