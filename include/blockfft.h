@@ -371,9 +371,11 @@ void fft_host_free(void *p);
 /* Host-link roofline of the streamer: copies `bytes`
  * between pinned host buffers and `device`, best of `reps` after a warm-up,
  * timed with CUDA events.  gbs[0] = H2D GB/s alone, gbs[1] = D2H alone,
- * gbs[2] / gbs[3] = H2D / D2H while both directions run at once.  Run it on
- * several GPUs from several threads at the same time for the aggregate
- * roofline.  Returns FFT_OK or FFT_E_ARG / FFT_E_DEVICE / FFT_E_CUDA.       */
+ * gbs[2] / gbs[3] = H2D / D2H while both directions run at once (best round),
+ * gbs[4] = GB/s each way sustained over all `reps` concurrent rounds (gbs
+ * holds 5 doubles).  Run it on several GPUs from several threads at the same
+ * time for the aggregate roofline.  Returns FFT_OK or FFT_E_ARG /
+ * FFT_E_DEVICE / FFT_E_CUDA.                                               */
 int fft_link_probe(int device, const void *host_src, void *host_dst, int64_t bytes, int reps, double *gbs);
 
 /* The streamer (fft_file*, fft_exec_host) caches its per-GPU resources

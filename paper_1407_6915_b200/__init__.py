@@ -414,10 +414,10 @@ class HostBuffer:
 
 def link_probe(device: int, src: HostBuffer, dst: HostBuffer, nbytes: int, reps: int = 3) -> dict:
     """fft_link_probe: H2D / D2H GB/s alone and concurrently (pinned buffers)."""
-    g = (ctypes.c_double * 4)()
+    g = (ctypes.c_double * 5)()
     _check(_lib.fft_link_probe(int(device), ctypes.c_void_p(src._p), ctypes.c_void_p(dst._p), int(nbytes),
                                int(reps), g))
-    return {"h2d": g[0], "d2h": g[1], "both_h2d": g[2], "both_d2h": g[3]}
+    return {"h2d": g[0], "d2h": g[1], "both_h2d": g[2], "both_d2h": g[3], "both_sustained": g[4]}
 
 
 def stream_release() -> int:

@@ -1,11 +1,17 @@
 """Command line: the whole method on a file, plus the partition plan.
 
   python -m paper_1407_6915_b200 fft IN OUT --record-len N [--ngpu G] [--inverse | --identity]
+                                  [--real | --hop H [--window hann|none]] [--direct-io]
                                   [--chunk-bytes B] [--force] [--report PATH]
+  python -m paper_1407_6915_b200 fan-out IN OUT --record-len N [--inverse] [--real | --hop H ...]
+        (one process per GPU under torchrun: every rank transforms its record range,
+         rank 0 renames; the multi-node form of fft, paper_1407_6915_b200.dist.fan_out)
   python -m paper_1407_6915_b200 partition --records R --gpus G
 
 `fft` is fft_file_ex (include/blockfft.h): IN is a headerless little-endian
-complex64 file split into records of N points (final record zero-padded,
+complex64 file (float32 with --real: packed half spectra out; --hop: the STFT
+of the file as one signal, frames every H samples, optional Hann window)
+split into records of N points (final record zero-padded,
 PAPER.md:49 / SURVEY.md §8(c) c6), every record is transformed on the GPUs and
 written at its own offset (PAPER.md:63 zero reducers, no merge step).  The
 stream statistics go to stdout (or --report) as JSON, messages to stderr.
@@ -50,7 +56,8 @@ def _cmd_fft(a) -> int:
             print(f"BLOCKFFT_BLOCK_SIZE must be an integer byte count: {env!r}", file=sys.stderr)
             return EXIT_VALIDATION
     try:
-        stats = bf.fft_file(a.input, a.output, a.record_len, a.ngpu, direction=direction, chunk_bytes=chunk)
+        stats = bf.fft_file(a.input, a.output, a.record_len, a.ngpu, direction=direction,
+                            options=_stream_options(a, chunk))
     except bf.FFTError as e:
         print(str(e), file=sys.stderr)
         return _exit_code(e.code)
@@ -61,6 +68,36 @@ def _cmd_fft(a) -> int:
             f.write(text + "\n")
     else:
         print(text)
+    return EXIT_OK
+
+
+def _stream_options(a, chunk):
+    import numpy as np
+    import paper_1407_6915_b200 as bf
+    window = None
+    if a.hop and a.window == "hann":
+        window = 0.5 - 0.5 * np.cos(2 * np.pi * np.arange(a.record_len) / a.record_len)
+    return bf.StreamOptions(chunk_bytes=chunk or 0, real=a.real, hop=a.hop or 0, window=window,
+                            direct_io=a.direct_io)
+
+
+def _cmd_fan_out(a) -> int:
+    import torch.distributed as dist
+    import paper_1407_6915_b200 as bf
+    from paper_1407_6915_b200 import dist as bd
+    info = bd.rank_info()
+    if info.world > 1 and not dist.is_initialized():
+        dist.init_process_group("gloo")
+    direction = bf.FFT_INVERSE if a.inverse else bf.FFT_FORWARD
+    try:
+        st = bd.fan_out(a.input, a.output, a.record_len, direction, options=_stream_options(a, a.chunk_bytes))
+    except bf.FFTError as e:
+        print(str(e), file=sys.stderr)
+        return _exit_code(e.code)
+    finally:
+        if info.world > 1 and dist.is_initialized():
+            dist.destroy_process_group()
+    print(json.dumps(st))
     return EXIT_OK
 
 
@@ -90,6 +127,22 @@ def main(argv=None) -> int:
     f.add_argument("--chunk-bytes", type=int, default=None)
     f.add_argument("--force", action="store_true")
     f.add_argument("--report", default=None)
+    k = f.add_mutually_exclusive_group()
+    k.add_argument("--real", action="store_true", help="records of N float32 samples (packed half spectra)")
+    k.add_argument("--hop", type=int, default=0, help="STFT: frames of N samples every HOP samples")
+    f.add_argument("--window", choices=["none", "hann"], default="none")
+    f.add_argument("--direct-io", action="store_true", help="O_DIRECT file I/O where supported")
+    fo = sub.add_parser("fan-out", help="this rank's record range of a file (torchrun: one process per GPU/node)")
+    fo.add_argument("input")
+    fo.add_argument("output")
+    fo.add_argument("--record-len", type=int, required=True)
+    fo.add_argument("--inverse", action="store_true")
+    fo.add_argument("--chunk-bytes", type=int, default=0)
+    k2 = fo.add_mutually_exclusive_group()
+    k2.add_argument("--real", action="store_true")
+    k2.add_argument("--hop", type=int, default=0)
+    fo.add_argument("--window", choices=["none", "hann"], default="none")
+    fo.add_argument("--direct-io", action="store_true")
     p = sub.add_parser("partition", help="the contiguous record range of every GPU")
     p.add_argument("--records", type=int, required=True)
     p.add_argument("--gpus", type=int, required=True)
@@ -97,7 +150,12 @@ def main(argv=None) -> int:
         a = ap.parse_args(argv)
     except SystemExit as e:       # argparse usage errors are validation errors
         return EXIT_VALIDATION if e.code else EXIT_OK
-    return _cmd_fft(a) if a.cmd == "fft" else _cmd_partition(a)
+    if a.cmd == "fft":
+        if a.identity and (a.real or a.hop):
+            print("--identity copies complex64 records: not with --real or --hop", file=sys.stderr)
+            return EXIT_VALIDATION
+        return _cmd_fft(a)
+    return _cmd_fan_out(a) if a.cmd == "fan-out" else _cmd_partition(a)
 
 
 if __name__ == "__main__":

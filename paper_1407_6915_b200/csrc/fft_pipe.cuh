@@ -339,14 +339,15 @@ __device__ __forceinline__ void red_relaxed_gpu(int* p, int v) {
     asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP = 16>
+template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP = 16, int NGRP = 1>
 struct Pipe2Cfg {
     static constexpr int N = N1 * N2;
-    static constexpr int NTC = COLS * Sched<N1, PP>::T;        // compute threads
+    static constexpr int NTC = COLS * Sched<N1, PP>::T;        // compute threads per group
     static_assert(ROWS * Sched<N2, PP>::T == NTC, "A and B tasks use the same compute warps");
     static_assert(Sched<N1, PP>::P == PP && Sched<N2, PP>::P == PP, "N1, N2 >= PP");
     static_assert(NTC % 32 == 0, "whole compute warps");
-    static constexpr int NT = NTC + 64;                          // + producer warp + release warp
+    static_assert(NGRP >= 1 && NGRP <= NSTAGE, "every group's end marker needs a stage of its own");
+    static constexpr int NT = NTC * NGRP + 64;                   // + producer warp + release warp
     static constexpr int TA = N2 / COLS, TB = N1 / ROWS;
     static constexpr int RSTRIDE = N2 + 2;                       // padded B-tile row (16-B multiple)
     static constexpr int TILE_A = COLS * N1, TILE_B = ROWS * RSTRIDE;
@@ -374,9 +375,9 @@ struct Pipe2Cfg {
 //              W_{N2 PP}^{t' q} * W_{PP^2}^{q s} from two small shared-memory
 //              tables — no global load on either task's critical path.
 enum { TW_TREE = 0, TW_TABLE = 1, TW_SPLIT = 2 };
-template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP, int TWM>
+template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP, int TWM, int NGRP = 1>
 constexpr size_t pipe2_smem() {
-    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>;
+    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP>;
     return CF::SMEM + (TWM == TW_SPLIT ? CF::SMEM_TW : 0);
 }
 
@@ -386,13 +387,17 @@ struct PipeTask {
     int tile;       // column tile (A) or row tile (B)
 };
 
-template <int N1, int N2, int COLS, int ROWS, bool INV, int NSTAGE, int PP = 16, int TWM = TW_TREE>
-__global__ void __launch_bounds__(Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>::NT,
-                                  Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>::MINB)
+// NGRP compute groups (NTC threads each, own named barrier) take tasks
+// k = g, g + NGRP, ... of the CTA's claimed sequence, each computing in the
+// stage its task was loaded into: NGRP tasks compute concurrently per CTA
+// while the producer stages the next (NSTAGE >= NGRP + 1 to overlap).
+template <int N1, int N2, int COLS, int ROWS, bool INV, int NSTAGE, int PP = 16, int TWM = TW_TREE, int NGRP = 1>
+__global__ void __launch_bounds__(Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP>::NT,
+                                  Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP>::MINB)
 k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, float2* __restrict__ ring,
         int64_t nrec, int* __restrict__ ctr, int S, int LAG, float scale, const float2* __restrict__ w_hi,
         const float2* __restrict__ w_lo, int w_lb) {
-    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>;
+    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP>;
     constexpr int LPP = ilog2(PP);
     constexpr int N = CF::N, TA = CF::TA, TB = CF::TB, NTC = CF::NTC, TILE = CF::TILE, RSTRIDE = CF::RSTRIDE;
     constexpr int TA1 = Sched<N1, PP>::T, TB2 = Sched<N2, PP>::T;
@@ -401,7 +406,7 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
     uint64_t* bars = reinterpret_cast<uint64_t*>(info + NSTAGE);   // full | empty | done
     const uint32_t full0 = smem_addr(bars), empty0 = smem_addr(bars + NSTAGE), done0 = smem_addr(bars + 2 * NSTAGE);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    constexpr int WP = NTC / 32, WR = NTC / 32 + 1;  // producer, release warps
+    constexpr int WP = NGRP * NTC / 32, WR = WP + 1;  // producer, release warps
     int* doneA = ctr + 1;
     int* doneB = ctr + 1 + S;
     const int64_t per_round = TA + TB;
@@ -422,6 +427,7 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
         // lane 0 claims, waits and arms the stage; the B-tile's ROWS row copies
         // are spread over the warp's lanes
         uint32_t k = 0;
+        int ends = 0;   // end markers staged (one per compute group)
         const uint64_t pol_stream = policy_evict_first();
         long long next = 0;
         if (lane == 0) next = atomicAdd(ctr, 1);  // the next claim is in flight while a task is staged
@@ -480,7 +486,11 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                     mbar_expect_tx(fb, (uint32_t)((d.kind == 0 ? CF::TILE_A : ROWS * N2) * sizeof(float2)));
                 }
             }
-            if (d.kind == 2) break;
+            if (d.kind == 2) {
+                if (++ends == NGRP) break;
+                ++k;
+                continue;
+            }
             __syncwarp();
             float2* stage = sm + (size_t)s * TILE;
             if (d.kind == 0) {
@@ -533,16 +543,19 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
         const TwoLevel W{w_hi, w_lo, w_lb, (uint32_t)(N - 1)};
         const ConstTw<N1, PP> tabA{};
         const ConstTw<N2, PP> tabB{};
-        const NamedBarrier bar{1, NTC};
+        const int grp = warp / (NTC / 32);
+        const int gtid = tid - grp * NTC;   // thread index within the group
+        const NamedBarrier bar{1 + grp, NTC};
         float2* tw_t = reinterpret_cast<float2*>(reinterpret_cast<char*>(sm) + CF::OFF_TW);   // T[q][s]
         float2* tw_b0 = tw_t + CF::TW_T;                                                       // WB0[t][q]
         if constexpr (TWM == TW_SPLIT) {
             // w_lo = WB0 [TB2][PP] then T [PP][PP]: copy into shared memory (T rows padded)
-            for (int i = tid; i < CF::TW_B0; i += NTC) tw_b0[i] = w_lo[i];
-            for (int i = tid; i < PP * PP; i += NTC) tw_t[(i / PP) * (PP + 1) + i % PP] = w_lo[CF::TW_B0 + i];
-            bar();
+            for (int i = tid; i < CF::TW_B0; i += NGRP * NTC) tw_b0[i] = w_lo[i];
+            for (int i = tid; i < PP * PP; i += NGRP * NTC) tw_t[(i / PP) * (PP + 1) + i % PP] = w_lo[CF::TW_B0 + i];
+            const NamedBarrier all{1 + NGRP, NGRP * NTC};
+            all();
         }
-        for (uint32_t k = 0;; ++k) {
+        for (uint32_t k = grp;; k += NGRP) {
             const uint32_t s = k % NSTAGE, u = k / NSTAGE;
             P2_T(ct0)
             mbar_wait(full0 + 8 * s, u & 1);
@@ -556,7 +569,7 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
             float2 v[PP];
             if (d.kind == 0) {
                 // ---------------- A: columns n2 of record r, FFT over n1, twiddle, -> ring
-                const int col = tid % COLS, t = tid / COLS;
+                const int col = gtid % COLS, t = gtid / COLS;
                 const int n2 = d.tile * COLS + col;
                 float2 f[LPP], w0;
                 if constexpr (TWM == TW_TREE) {
@@ -606,11 +619,11 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 for (int q = 0; q < PP; ++q) dst[(int64_t)q * TA1 * N2] = v[q];
             } else {
                 // ---------------- B: rows k1 of record r, FFT over n2, -> X[k1 + N1 k2]
-                const int col = tid % ROWS, t = tid / ROWS;
+                const int col = gtid % ROWS, t = gtid / ROWS;
                 const int k0 = d.tile * ROWS;
                 {   // the tile's ring rows are staged: drop them from L2 (no write-back)
                     const char* rows = reinterpret_cast<const char*>(ring + (int64_t)slot * N + (int64_t)k0 * N2);
-                    for (int i = tid; i < ROWS * N2 * 8 / 128; i += NTC) l2_discard128(rows + 128 * i);
+                    for (int i = gtid; i < ROWS * N2 * 8 / 128; i += NTC) l2_discard128(rows + 128 * i);
                 }
                 if constexpr (TWM == TW_SPLIT) {
                     // the W_{N2 PP}^{n2 qa} part, n2 = t + TB2 s, qa = k1 / TA1, applied

@@ -29,9 +29,10 @@ def fill_random(t, seed: int, first_sample: int = 0, stream=None):
     [first_sample, first_sample + t.numel()) of stream ``seed``."""
     import torch
     assert t.is_cuda and t.dtype == torch.complex64 and t.is_contiguous()
-    s = stream if stream is not None else torch.cuda.current_stream()
-    rc = _load().synth_fill_random(ctypes.c_void_p(t.data_ptr()), int(first_sample), t.numel(),
-                                   ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), ctypes.c_void_p(s.cuda_stream))
+    with torch.cuda.device(t.device):     # launch on the tensor's own GPU
+        s = stream if stream is not None else torch.cuda.current_stream(t.device)
+        rc = _load().synth_fill_random(ctypes.c_void_p(t.data_ptr()), int(first_sample), t.numel(),
+                                       ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), ctypes.c_void_p(s.cuda_stream))
     if rc != 0:
         raise RuntimeError(f"synth_fill_random failed: cudaError {rc}")
     return t

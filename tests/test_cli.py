@@ -72,3 +72,39 @@ def test_cli_file_transform_and_io_errors(tmp_path):
     assert rc == 3 and "cannot open" in err
     rc, _, _ = run_cli("fft", str(src), str(tmp_path / "o4"), "--record-len", str(n), "--ngpu", "99")
     assert rc == 2
+
+
+@pytest.mark.gpu
+def test_cli_real_and_stft(tmp_path):
+    n = 1024
+    x = synth.random_samples(23, 0, 9 * n // 2).view(np.float32)
+    src, dst = tmp_path / "in.f32", tmp_path / "out.c64"
+    x.astype("<f4").tofile(src)
+    rc, out, err = run_cli("fft", str(src), str(dst), "--record-len", str(n), "--real")
+    assert rc == 0, err
+    y = np.fromfile(dst, "<c8").reshape(-1, n // 2)
+    full = oracle.records_c64(x.reshape(-1, n).astype(np.complex64), oracle.FORWARD)
+    packed = full[:, : n // 2].copy()
+    packed[:, 0] = full[:, 0].real + 1j * full[:, n // 2].real
+    assert np.all(oracle.rel_l2(y, packed) <= oracle.tolerance(n))
+    sig = synth.random_samples(29, 0, 5000)
+    s2, d2 = tmp_path / "sig.c64", tmp_path / "stft.c64"
+    sig.astype("<c8").tofile(s2)
+    rc, out, err = run_cli("fft", str(s2), str(d2), "--record-len", "256", "--hop", "128", "--window", "hann")
+    assert rc == 0, err
+    assert json.loads(out)["stats"]["records"] == 1 + -(-(5000 - 256) // 128)
+    rc, _, err = run_cli("fft", str(s2), str(tmp_path / "bad"), "--record-len", "256", "--hop", "128", "--identity")
+    assert rc == 1
+
+
+@pytest.mark.gpu
+def test_cli_fan_out_single_process(tmp_path):
+    n = 2048
+    s = synth.random_samples(37, 0, 11 * n)
+    src, dst, ref = tmp_path / "in.c64", tmp_path / "out.c64", tmp_path / "ref.c64"
+    s.astype("<c8").tofile(src)
+    rc, out, err = run_cli("fan-out", str(src), str(dst), "--record-len", str(n))
+    assert rc == 0, err
+    assert json.loads(out)["count"] == 11
+    rc, _, err = run_cli("fft", str(src), str(ref), "--record-len", str(n))
+    assert rc == 0 and dst.read_bytes() == ref.read_bytes()

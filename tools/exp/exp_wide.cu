@@ -9,24 +9,26 @@ using namespace bfft;
 
 struct Cfg { const void* fn; int threads; size_t smem; int cols, rows, stages, twm, boxr, pp; const char* name; };
 
-template <int COLS, int ROWS, int NST, int PP, int TWM>
+template <int COLS, int ROWS, int NST, int PP, int TWM, int NGRP = 1>
 static Cfg mk(const char* name) {
-    using CF = Pipe2Cfg<256, 256, COLS, ROWS, NST, PP>;
-    return Cfg{(const void*)&k_pipe2<256, 256, COLS, ROWS, false, NST, PP, TWM>, CF::NT,
-               pipe2_smem<256, 256, COLS, ROWS, NST, PP, TWM>(), COLS, ROWS, NST, TWM, CF::BOXR, PP, name};
+    using CF = Pipe2Cfg<256, 256, COLS, ROWS, NST, PP, NGRP>;
+    return Cfg{(const void*)&k_pipe2<256, 256, COLS, ROWS, false, NST, PP, TWM, NGRP>, CF::NT,
+               pipe2_smem<256, 256, COLS, ROWS, NST, PP, TWM, NGRP>(), COLS, ROWS, NST, TWM, CF::BOXR, PP, name};
 }
 static Cfg table(int i) {
     switch (i) {
-        case 0: return mk<16, 16, 2, 32, TW_TABLE>("c16 s2 p32 table (r01 default)");
-        case 1: return mk<16, 16, 2, 32, TW_SPLIT>("c16 s2 p32 split");
-        case 2: return mk<16, 16, 2, 16, TW_SPLIT>("c16 s2 p16 split");
-        case 3: return mk<16, 16, 2, 16, TW_TABLE>("c16 s2 p16 table");
-        case 4: return mk<16, 16, 2, 32, TW_TREE>("c16 s2 p32 tree");
-        case 5: return mk<16, 16, 2, 16, TW_TREE>("c16 s2 p16 tree");
+        case 0: return mk<16, 16, 2, 32, TW_SPLIT>("c16 s2 p32 split g1 (default)");
+        case 1: return mk<16, 16, 3, 32, TW_SPLIT, 2>("c16 s3 p32 split g2");
+        case 2: return mk<16, 16, 4, 32, TW_SPLIT, 3>("c16 s4 p32 split g3");
+        case 3: return mk<16, 16, 2, 32, TW_SPLIT, 2>("c16 s2 p32 split g2");
+        case 4: return mk<16, 16, 5, 32, TW_SPLIT, 4>("c16 s5 p32 split g4");
+        case 5: return mk<16, 16, 3, 32, TW_SPLIT, 3>("c16 s3 p32 split g3");
+        case 6: return mk<16, 16, 3, 16, TW_SPLIT, 2>("c16 s3 p16 split g2");
+        case 7: return mk<32, 32, 3, 32, TW_SPLIT, 2>("c32 s3 p32 split g2");
         default: return Cfg{nullptr, 0, 0, 0, 0, 0, 0, 0, 0, nullptr};
     }
 }
-extern "C" int exp_ncfg() { return 6; }
+extern "C" int exp_ncfg() { return 8; }
 // the constant-memory Stockham twiddles of this translation unit (same table as plan.cu builds)
 static void stockham_table(int L, std::vector<float2>& out, int P) {
     out.clear();

@@ -38,13 +38,13 @@ import paper_1407_6915_b200 as bf  # noqa: E402
 import synth  # noqa: E402
 
 
-def probe(gpus, nbytes):
+def probe(gpus, nbytes, reps=3):
     bufs = {g: (bf.HostBuffer(nbytes // 8, 1, g), bf.HostBuffer(nbytes // 8, 1, g)) for g in gpus}
     res, bar = {}, threading.Barrier(len(gpus))
 
     def run(g):
         bar.wait()
-        res[g] = bf.link_probe(g, bufs[g][0], bufs[g][1], nbytes, reps=3)
+        res[g] = bf.link_probe(g, bufs[g][0], bufs[g][1], nbytes, reps=reps)
     th = [threading.Thread(target=run, args=(g,)) for g in gpus]
     [t.start() for t in th]
     [t.join() for t in th]
@@ -80,7 +80,8 @@ def main():
             rows.append({"gpus": gcount, "skipped": f"only {ndev} GPUs visible"})
             continue
         gpus = list(range(gcount))
-        link = probe(gpus, 1 << 30)
+        link = probe(gpus, 1 << 30)                   # burst: best of 3 concurrent rounds
+        link_sus = probe(gpus, 1 << 30, reps=200)     # sustained: ~5-10 s of back-to-back rounds
         ins, outs, opts, stats = {}, {}, {}, {}
         # taps: one record per GiB of the whole logical stream, in each GPU's share
         tap_all = np.arange(0, total, (1 << 30) // rb, dtype=np.int64)
@@ -127,12 +128,16 @@ def main():
             ntaps += len(rid)
         agg_h2d = sum(link[g]["both_h2d"] for g in gpus)
         agg_d2h = sum(link[g]["both_d2h"] for g in gpus)
+        agg_sus = sum(link_sus[g]["both_sustained"] for g in gpus)
         each_way = moved / slowest / 1e9
         row = {"gpus": gcount, "n": n, "logical_bytes": total * rb, "records": total, "seconds": slowest,
                "wall_s": wall, "records_per_s": total / slowest, "GBps_each_way": each_way,
                "link_roofline": {"per_gpu": link, "aggregate_concurrent_h2d": agg_h2d,
                                  "aggregate_concurrent_d2h": agg_d2h},
+               "link_sustained": {"per_gpu": {g: link_sus[g]["both_sustained"] for g in gpus},
+                                  "aggregate_each_way": agg_sus},
                "frac_of_link_h2d": each_way / agg_h2d, "frac_of_link_d2h": each_way / agg_d2h,
+               "frac_of_sustained_link": each_way / agg_sus,
                "numa_nodes": {g: res[g][0]["numa_node"] for g in gpus},
                "busy": {g: {s: res[g][0][s] / res[g][1] for s in ("h2d_s", "fft_s", "d2h_s")} for g in gpus},
                "taps": ntaps, "taps_not_bit_identical": bad,
