@@ -105,7 +105,11 @@ typedef struct fft_plan_opts {
                          FFT_VARIANT_CLUSTER 1 k_cluster1 (single buffer),
                                              2 k_cluster2 (pipelined),
                                              3 k_cluster (TMA-staged)          */
-    int config;       /* k_pipe3 (stages, groups, claim batch) set, 0..4     */
+    int config;       /* configuration inside the implementation, 0 = default:
+                         k_pipe2 1 = one compute group / two stages, 2 = two
+                         groups / three stages, 3 = two groups / three 64 KiB
+                         stages (2^17, 2^18); k_pipe3 0..4 = (stages, groups,
+                         claim batch) sets                                     */
     int cluster_size; /* FFT_VARIANT_CLUSTER: CTAs per cluster, 0 = default */
     int ring_records; /* FFT_VARIANT_PIPE: L2 ring slots S, 0 = sized from the
                          tasks in flight (capped at 96 MiB); > 0 forces

@@ -79,6 +79,13 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+// L2 prefetch of one TMA box (no shared memory, no barrier)
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* tmap, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmap)),
+                 "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
 __device__ __forceinline__ void tma_load_3d_hint(uint32_t dst, const CUtensorMap* tmap, int c0, int c1, int c2,
                                                  uint32_t bar, uint64_t pol) {
     asm volatile(
@@ -391,7 +398,8 @@ struct PipeTask {
 // k = g, g + NGRP, ... of the CTA's claimed sequence, each computing in the
 // stage its task was loaded into: NGRP tasks compute concurrently per CTA
 // while the producer stages the next (NSTAGE >= NGRP + 1 to overlap).
-template <int N1, int N2, int COLS, int ROWS, bool INV, int NSTAGE, int PP = 16, int TWM = TW_TREE, int NGRP = 1>
+template <int N1, int N2, int COLS, int ROWS, bool INV, int NSTAGE, int PP = 16, int TWM = TW_TREE, int NGRP = 1,
+          int CB = 1, bool PF = false>
 __global__ void __launch_bounds__(Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP>::NT,
                                   Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP>::MINB)
 k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, float2* __restrict__ ring,
@@ -403,8 +411,9 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
     constexpr int TA1 = Sched<N1, PP>::T, TB2 = Sched<N2, PP>::T;
     extern __shared__ __align__(128) float2 sm[];
     PipeTask* info = reinterpret_cast<PipeTask*>(sm + (size_t)TILE * NSTAGE);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(info + NSTAGE);   // full | empty | done
+    uint64_t* bars = reinterpret_cast<uint64_t*>(info + NSTAGE);   // full | empty | done | sfree
     const uint32_t full0 = smem_addr(bars), empty0 = smem_addr(bars + NSTAGE), done0 = smem_addr(bars + 2 * NSTAGE);
+    const uint32_t sfree0 = smem_addr(bars + 3 * NSTAGE);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr int WP = NGRP * NTC / 32, WR = WP + 1;  // producer, release warps
     int* doneA = ctr + 1;
@@ -416,7 +425,8 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
         for (int i = 0; i < NSTAGE; ++i) {
             mbar_init(full0 + 8 * i, 1);
             mbar_init(empty0 + 8 * i, 1);       // the release warp frees a stage
-            mbar_init(done0 + 8 * i, NTC / 32); // one arrival per compute warp
+            mbar_init(done0 + 8 * i, NTC / 32); // one arrival per compute warp: stores issued
+            mbar_init(sfree0 + 8 * i, NTC / 32);// one arrival per compute warp: stage read for the last time
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -429,31 +439,56 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
         uint32_t k = 0;
         int ends = 0;   // end markers staged (one per compute group)
         const uint64_t pol_stream = policy_evict_first();
-        long long next = 0;
-        if (lane == 0) next = atomicAdd(ctr, 1);  // the next claim is in flight while a task is staged
+        // Tasks are claimed CB at a time (one atomic per batch, the next batch's
+        // claim in flight while this one is staged); consecutive tasks mostly
+        // share a record, so a dependency already seen satisfied is not waited
+        // for again (the last (counter, value) acquired is cached).
+        long long base = 0, nextb = 0;
+        int sub = 0;
+        const int* dep_ptr = nullptr;
+        int dep_seen = 0;
+        auto decode = [&](long long task, PipeTask& t) -> bool {   // false: not a task of this launch
+            if (task >= total) {
+                t.kind = 2;
+                t.rec = 0;
+                t.tile = 0;
+                return true;
+            }
+            const long long round = task / per_round;
+            const int o = (int)(task - round * per_round);
+            if (o < TA) {
+                t.kind = 0;
+                t.rec = round;
+                t.tile = o;
+                return round < nrec;
+            }
+            t.kind = 1;
+            t.rec = round - LAG;
+            t.tile = o - TA;
+            return t.rec >= 0 && t.rec < nrec;
+        };
+        if (lane == 0) {
+            base = atomicAdd(ctr, CB);
+            if (base < total) nextb = atomicAdd(ctr, CB);
+        }
         for (;;) {
             PipeTask d;
             bool valid = true;
             if (lane == 0) {
-                const long long task = next;
-                if (task < total) next = atomicAdd(ctr, 1);
-                if (task >= total) {
-                    d.kind = 2;
-                    d.rec = 0;
-                    d.tile = 0;
-                } else {
-                    const long long round = task / per_round;
-                    const int o = (int)(task - round * per_round);
-                    if (o < TA) {
-                        d.kind = 0;
-                        d.rec = round;
-                        d.tile = o;
-                        valid = round < nrec;
-                    } else {
-                        d.kind = 1;
-                        d.rec = round - LAG;
-                        d.tile = o - TA;
-                        valid = d.rec >= 0 && d.rec < nrec;
+                const long long task = base + sub;
+                if (++sub == CB) {
+                    sub = 0;
+                    base = nextb;
+                    if (base < total) nextb = atomicAdd(ctr, CB);
+                }
+                valid = decode(task, d);
+                if constexpr (PF) {
+                    // pull the next A-tile from HBM into L2 while this task waits for its stage
+                    PipeTask nx;
+                    if (valid && d.kind != 2 && decode(base + sub, nx) && nx.kind == 0) {
+#pragma unroll 1
+                        for (int r0 = 0; r0 < N1; r0 += CF::BOXR)
+                            tma_prefetch_3d(&tmap_in, nx.tile * COLS, r0, (int)nx.rec);
                     }
                 }
             }
@@ -473,13 +508,20 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 } else {
                     const int slot = (int)(d.rec % S), gen = (int)(d.rec / S);
 #ifndef BFFT_PIPE_NODEPS  // (experiments only: tools/exp measures the kernel without its waits)
+                    const int* dp = nullptr;
+                    int target = 0;
                     if (d.kind == 0) {
 #ifndef BFFT_PIPE_NOWAR   // (mutation experiment only: tools/exp/stress_mutant.py)
-                        if (gen > 0) wait_geq(doneB + slot, gen * TB);   // ring slot free (WAR)
+                        if (gen > 0) dp = doneB + slot, target = gen * TB;   // ring slot free (WAR)
 #endif
                     } else {
-                        wait_geq(doneA + slot, (gen + 1) * TA);          // column FFTs published
-                        fence_proxy_async_global();   // generic ring stores -> this bulk-copy read
+                        dp = doneA + slot, target = (gen + 1) * TA;          // column FFTs published
+                    }
+                    if (dp && !(dp == dep_ptr && target <= dep_seen)) {
+                        dep_seen = wait_geq_v(dp, target);
+                        dep_ptr = dp;
+                        // generic ring stores acquired here -> this thread's later bulk-copy reads
+                        if (d.kind == 1) fence_proxy_async_global();
                     }
 #endif
                     info[s] = d;
@@ -518,10 +560,11 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 if (d.kind == 2) break;
                 P2_T(rt0)
                 BFFT_STRESS_DELAY(11);
+                mbar_wait(sfree0 + 8 * s, u & 1);
+                mbar_arrive(empty0 + 8 * s);   // stage reusable: its last exchange has been read
                 mbar_wait(done0 + 8 * s, u & 1);
                 P2_T(rt1)
                 BFFT_STRESS_DELAY(12);
-                mbar_arrive(empty0 + 8 * s);   // stage reusable (compute warps are past it)
 #ifndef BFFT_PIPE_NODEPS
 #ifndef BFFT_PIPE_REDREL
                 fence_acq_rel_gpu();            // their stores, observed through done[s], become visible
@@ -590,6 +633,8 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
 #ifndef BFFT_PIPE_NOFENCE
                 fence_proxy_async_smem();   // last generic access of the stage: before its next TMA refill
 #endif
+                __syncwarp();
+                if (lane == 0) mbar_arrive(sfree0 + 8 * s);   // the producer may refill the stage now
 #ifdef BFFT_PIPE_NOTW   // (experiments only: the kernel without its four-step twiddle; results wrong)
                 if constexpr (true) {
                 } else
@@ -649,6 +694,8 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
 #ifndef BFFT_PIPE_NOFENCE
                 fence_proxy_async_smem();   // last generic access of the stage: before its next bulk refill
 #endif
+                __syncwarp();
+                if (lane == 0) mbar_arrive(sfree0 + 8 * s);   // the producer may refill the stage now
                 float2* dst = out + r * N + k0 + col + (int64_t)t * N1;
 #pragma unroll
                 for (int q = 0; q < PP; ++q)

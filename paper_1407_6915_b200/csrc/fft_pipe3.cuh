@@ -81,13 +81,6 @@ __device__ __forceinline__ int ld_acquire_cta_s(const int* p) {
 __device__ __forceinline__ void st_release_cta_s(int* p, int v) {
     asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
 }
-// L2 prefetch of one TMA box (no shared memory, no barrier)
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* tmap, int c0, int c1, int c2) {
-    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
-                     reinterpret_cast<uint64_t>(tmap)),
-                 "r"(c0), "r"(c1), "r"(c2)
-                 : "memory");
-}
 __device__ __forceinline__ int ld_volatile_s(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 
 template <int N1, int N2, int COLS, int ROWS, bool INV, int NS, int G, int PP = 32, int CB = 4, bool PF = false>

@@ -6,9 +6,9 @@
 
 using namespace bfft;
 
-template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP = 16, int TWM = TW_SPLIT>
+template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP = 16, int TWM = TW_SPLIT, int NGRP = 1>
 static PipeChoice pipe2_kernel(bool inv) {
-    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP>;
+    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP>;
     PipeChoice ch;
     ch.n1 = N1;
     ch.n2 = N2;
@@ -17,12 +17,12 @@ static PipeChoice pipe2_kernel(bool inv) {
     ch.impl = 2;
     ch.stages = NSTAGE;
     ch.boxr = CF::BOXR;
-    ch.k.fn = inv ? (const void*)&k_pipe2<N1, N2, COLS, ROWS, true, NSTAGE, PP, TWM>
-                  : (const void*)&k_pipe2<N1, N2, COLS, ROWS, false, NSTAGE, PP, TWM>;
+    ch.k.fn = inv ? (const void*)&k_pipe2<N1, N2, COLS, ROWS, true, NSTAGE, PP, TWM, NGRP>
+                  : (const void*)&k_pipe2<N1, N2, COLS, ROWS, false, NSTAGE, PP, TWM, NGRP>;
     ch.twm = TWM;
     ch.pp = PP;
     ch.k.threads = CF::NT;
-    ch.k.smem = pipe2_smem<N1, N2, COLS, ROWS, NSTAGE, PP, TWM>();
+    ch.k.smem = pipe2_smem<N1, N2, COLS, ROWS, NSTAGE, PP, TWM, NGRP>();
     return ch;
 }
 template <int N1, int N2, int COLS, int ROWS> static PipeChoice pipe_kernel(bool inv) {
@@ -39,19 +39,46 @@ template <int N1, int N2, int COLS, int ROWS> static PipeChoice pipe_kernel(bool
 }
 // Pipelined four-step configurations per size: N = N1 * N2 (N1 >= N2), A-tile
 // COLS columns, B-tile ROWS rows, NSTAGE staged tiles per CTA, PP points per
-// thread, TWM = how the four-step twiddle is applied (TW_SPLIT everywhere:
-// fft_pipe.cuh; profiles/r02_twiddle_split.txt).  The defaults
-// (impl 0) are the fastest measured on B200 (profiles/r01_variants_*,
-// r01_pipe3_*, r01_pipe2_large.txt, r01_twiddle_table.txt): k_pipe3 (compute
-// groups, early stage release) at 2^19 and 2^20, warp-specialised k_pipe2
-// elsewhere (radix-32 engines at 2^15..2^20, radix-16 with 64 KiB tiles at
-// 2^21..2^22).  impl 1 = k_pipe, 2 = k_pipe2, 3 = k_pipe3 select the
-// alternatives explicitly (fft_plan_opts::impl; parity-tested in
+// thread, TWM = how the four-step twiddle is applied (TW_SPLIT except at 2^18
+// one-group: fft_pipe.cuh; profiles/r02_twiddle_split.txt), NGRP compute
+// groups per CTA.  The default (impl 0) is the warp-specialised k_pipe2 at
+// every size, in its fastest measured configuration (profiles/r02_pipe2_groups.txt:
+// radix-32 engines at 2^15..2^20, radix-16 with 64 KiB tiles at 2^21..2^22);
+// impl 1 = k_pipe, 2 = k_pipe2, 3 = k_pipe3 select the alternatives
+// explicitly (fft_plan_opts::impl / config; parity-tested in
 // tests/test_gpu_parity.py).
 PipeChoice pick_pipe(int log2n, bool inv, int impl, int config) {
-    if (impl == 0) impl = (log2n >= 19 && log2n <= 20) ? 3 : 2;
+    if (impl == 0) impl = 2;
     if (impl == 3) return pick_pipe3(log2n, inv, config);
-    if (impl == 2) {
+    // k_pipe2 configurations (fft_plan_opts::config): 1 = one compute group over two
+    // stages (three CTAs per SM at 32 KiB tiles), 2 = two groups over three stages,
+    // 3 = two groups over three 64 KiB stages of 16-wide tiles; 0 = the fastest
+    // measured per size (profiles/r02_pipe2_groups.txt): 2 at 2^15..2^17 and
+    // 2^19..2^20, 3 at 2^18, 1 elsewhere
+    if (impl == 2 && config == 0)
+        config = (log2n == 18) ? 3 : ((log2n >= 15 && log2n <= 20) ? 2 : 1);
+    if (impl == 2 && config == 3) {
+        // two groups, three 64 KiB stages of 16-wide tiles (one CTA per SM)
+        switch (log2n) {
+            case 17: return pipe2_kernel<512, 256, 16, 32, 3, 32, TW_SPLIT, 2>(inv);
+            case 18: return pipe2_kernel<512, 512, 16, 16, 3, 32, TW_SPLIT, 2>(inv);
+            default: return PipeChoice{};
+        }
+    }
+    if (impl == 2 && config == 2) {
+        // two compute groups per CTA over three stages (two CTAs per SM: 16 compute warps)
+        switch (log2n) {
+            case 14: return pipe2_kernel<128, 128, 16, 16, 3, 16, TW_SPLIT, 2>(inv);
+            case 15: return pipe2_kernel<256, 128, 16, 32, 3, 32, TW_SPLIT, 2>(inv);
+            case 16: return pipe2_kernel<256, 256, 16, 16, 3, 32, TW_SPLIT, 2>(inv);
+            case 17: return pipe2_kernel<512, 256, 8, 16, 3, 32, TW_SPLIT, 2>(inv);
+            case 18: return pipe2_kernel<512, 512, 8, 8, 3, 32, TW_TREE, 2>(inv);
+            case 19: return pipe2_kernel<1024, 512, 8, 16, 3, 32, TW_SPLIT, 2>(inv);
+            case 20: return pipe2_kernel<1024, 1024, 8, 8, 3, 32, TW_SPLIT, 2>(inv);
+            default: return PipeChoice{};
+        }
+    }
+    if (impl == 2 && config == 1) {
         switch (log2n) {
             case 13: return pipe2_kernel<128, 64, 16, 32, 2, 16>(inv);
             case 14: return pipe2_kernel<128, 128, 16, 16, 2, 16>(inv);
@@ -68,7 +95,7 @@ PipeChoice pick_pipe(int log2n, bool inv, int impl, int config) {
             default: return PipeChoice{};
         }
     }
-    if (impl != 1) return PipeChoice{};
+    if (impl != 1 || config != 0) return PipeChoice{};
     switch (log2n) {
         case 13: return pipe_kernel<128, 64, 16, 32>(inv);
         case 14: return pipe_kernel<128, 128, 16, 16>(inv);

@@ -248,6 +248,16 @@ def test_pipe_implementations(impl, n):
     check(x, bf.FFT_INVERSE, bf.VARIANT_PIPE, impl=impl)
 
 
+@pytest.mark.parametrize("cfg,n", [(1, 1 << 13), (1, 1 << 15), (1, 1 << 16), (1, 1 << 18), (1, 1 << 20),
+                                   (2, 1 << 14), (2, 1 << 16), (2, 1 << 19), (3, 1 << 17), (3, 1 << 18)])
+def test_pipe2_configurations(cfg, n):
+    # k_pipe2 structures: one group / two stages, two groups / three stages, 64 KiB tiles
+    b = 5 if n >= (1 << 19) else 33
+    x = synth.random_records(81 + cfg, n, 0, b)
+    check(x, bf.FFT_FORWARD, bf.VARIANT_PIPE, impl=2, config=cfg)
+    check(x, bf.FFT_INVERSE, bf.VARIANT_PIPE, impl=2, config=cfg)
+
+
 @pytest.mark.parametrize("cfg,n", [(0, 1 << 15), (1, 1 << 16), (2, 1 << 16), (3, 1 << 17), (4, 1 << 16),
                                    (2, 1 << 18), (0, 1 << 19), (1, 1 << 20), (0, 1 << 20), (2, 1 << 20),
                                    (3, 1 << 19)])
@@ -260,7 +270,7 @@ def test_pipe3_configurations(cfg, n):
     check(x, bf.FFT_INVERSE, bf.VARIANT_PIPE, impl=3, config=cfg)
 
 
-@pytest.mark.parametrize("impl,cfg", [(3, 0), (3, 2), (2, 0), (1, 0)])
+@pytest.mark.parametrize("impl,cfg", [(3, 0), (3, 2), (2, 0), (2, 1), (1, 0)])
 def test_pipe_ring_forced_small(impl, cfg):
     # a ring forced down to LAG + 1 slots: every record reuses a slot many times
     # (WAR waits on every A-task), claim batches across record boundaries

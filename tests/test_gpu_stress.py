@@ -54,6 +54,8 @@ CASES = [
     (1 << 14, None, {}, True),
     (1 << 16, 17, dict(ring_lag=3, ring_records=4), True),
     (1 << 16, 17, dict(impl=1, ring_lag=3, ring_records=4), False),
+    (1 << 16, 17, dict(impl=2, config=1, ring_lag=3, ring_records=4), True),
+    (1 << 18, 11, dict(impl=2, config=3, ring_lag=2, ring_records=3), False),
     (1 << 16, 17, dict(impl=3, ring_lag=3, ring_records=4), True),
     (1 << 16, 17, dict(impl=3, config=2, ring_lag=3, ring_records=4), False),
     (1 << 17, 11, dict(ring_lag=2, ring_records=3), False),

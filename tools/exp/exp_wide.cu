@@ -7,25 +7,25 @@
 #include <vector>
 using namespace bfft;
 
-struct Cfg { const void* fn; int threads; size_t smem; int cols, rows, stages, twm, boxr, pp; const char* name; };
+struct Cfg { const void* fn; int threads; size_t smem; int cols, rows, stages, twm, boxr, pp; const char* name; int cb; };
 
-template <int COLS, int ROWS, int NST, int PP, int TWM, int NGRP = 1>
+template <int COLS, int ROWS, int NST, int PP, int TWM, int NGRP = 1, int CB = 1, bool PF = false>
 static Cfg mk(const char* name) {
     using CF = Pipe2Cfg<256, 256, COLS, ROWS, NST, PP, NGRP>;
-    return Cfg{(const void*)&k_pipe2<256, 256, COLS, ROWS, false, NST, PP, TWM, NGRP>, CF::NT,
-               pipe2_smem<256, 256, COLS, ROWS, NST, PP, TWM, NGRP>(), COLS, ROWS, NST, TWM, CF::BOXR, PP, name};
+    return Cfg{(const void*)&k_pipe2<256, 256, COLS, ROWS, false, NST, PP, TWM, NGRP, CB, PF>, CF::NT,
+               pipe2_smem<256, 256, COLS, ROWS, NST, PP, TWM, NGRP>(), COLS, ROWS, NST, TWM, CF::BOXR, PP, name, CB};
 }
 static Cfg table(int i) {
     switch (i) {
-        case 0: return mk<16, 16, 2, 32, TW_SPLIT>("c16 s2 p32 split g1 (default)");
-        case 1: return mk<16, 16, 3, 32, TW_SPLIT, 2>("c16 s3 p32 split g2");
-        case 2: return mk<16, 16, 4, 32, TW_SPLIT, 3>("c16 s4 p32 split g3");
-        case 3: return mk<16, 16, 2, 32, TW_SPLIT, 2>("c16 s2 p32 split g2");
-        case 4: return mk<16, 16, 5, 32, TW_SPLIT, 4>("c16 s5 p32 split g4");
-        case 5: return mk<16, 16, 3, 32, TW_SPLIT, 3>("c16 s3 p32 split g3");
-        case 6: return mk<16, 16, 3, 16, TW_SPLIT, 2>("c16 s3 p16 split g2");
-        case 7: return mk<32, 32, 3, 32, TW_SPLIT, 2>("c32 s3 p32 split g2");
-        default: return Cfg{nullptr, 0, 0, 0, 0, 0, 0, 0, 0, nullptr};
+        case 0: return mk<16, 16, 2, 32, TW_SPLIT>("c16 s2 g1 (default)");
+        case 1: return mk<16, 16, 3, 32, TW_SPLIT, 2>("c16 s3 g2");
+        case 2: return mk<8, 8, 6, 32, TW_SPLIT, 4>("c8 s6 g4");
+        case 3: return mk<8, 8, 5, 32, TW_SPLIT, 4>("c8 s5 g4");
+        case 4: return mk<8, 8, 6, 32, TW_SPLIT, 3>("c8 s6 g3");
+        case 5: return mk<8, 8, 4, 32, TW_SPLIT, 2>("c8 s4 g2");
+        case 6: return mk<8, 8, 3, 32, TW_SPLIT, 2>("c8 s3 g2");
+        case 7: return mk<16, 16, 3, 32, TW_SPLIT, 2, 2>("c16 s3 g2 cb2");
+        default: return Cfg{nullptr, 0, 0, 0, 0, 0, 0, 0, 0, nullptr, 1};
     }
 }
 extern "C" int exp_ncfg() { return 8; }
@@ -69,7 +69,7 @@ extern "C" float exp_run(int i, const void* in, void* out, void* ring, int* ctr,
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, c.fn, c.threads, c.smem);
     if (occ < 1) return -2.f;
     const int resident = occ * 148, per_round = 256 / c.cols + 256 / c.rows;
-    const long long inflight = (long long)resident * (c.stages + 1);
+    const long long inflight = (long long)resident * (c.stages + c.cb);
     const long long rounds = (inflight + per_round - 1) / per_round;
     int LAG = (int)(3 * rounds / 2 + 1);
     int S = (int)(LAG + 2 * rounds + 1);
