@@ -46,4 +46,9 @@ for i in cfgs:
     err = float(((y[:8].to(torch.complex128) - ref).abs().pow(2).sum(1).sqrt() / ref.abs().pow(2).sum(1).sqrt()).max())
     last = float(((torch.fft.fft(x[-2:].to(torch.complex128)) - y[-2:].to(torch.complex128)).abs().max()))
     gbs = 16.0 * n * b / (ms * 1e-3) / 1e9 if ms > 0 else 0
+    if hasattr(lib, "exp_prof_read"):
+        pr = (ctypes.c_ulonglong * 32)(); lib.exp_prof_read(pr)
+        na, nb = max(pr[22], 1), max(pr[23], 1)
+        print(f"   per task (cycles, all reps): A wait {pr[18]/na:.0f} work {pr[19]/na:.0f} | B wait {pr[20]/nb:.0f} work {pr[21]/nb:.0f}"
+              f" | release: wait done {pr[16]/(na+nb):.0f} fence+red {pr[17]/(na+nb):.0f}")
     print(f"{lib.exp_name(i).decode():32s} occ={occ.value} S={S.value}: {ms:.3f} ms {gbs:.0f} GB/s ({gbs/peak:.1%}) err={err:.2e} lastabs={last:.2e}", flush=True)
