@@ -34,7 +34,8 @@ def parse_ncu(path, lo, hi):
             continue
         d = launches.setdefault(int(r[iid]), {"kernel": r[ik]})
         d[r[im]] = float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
-    ordered = [launches[i] for i in sorted(launches)]
+    ours = ("k_rows", "k_pipe", "k_cluster", "k_fs_", "k_copy")
+    ordered = [launches[i] for i in sorted(launches) if any(o in launches[i]["kernel"] for o in ours)]
     out = {}
     for j, k in enumerate(range(lo, hi + 1)):
         if 2 * j + 1 < len(ordered):
@@ -49,10 +50,23 @@ def main():
     ap.add_argument("--gib", type=float, default=4.0)
     ap.add_argument("--ncu-csv", default=None)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--merge", default=None, help="add the ncu DRAM bytes to the rows of an earlier --json run")
     a = ap.parse_args()
     ncu = parse_ncu(a.ncu_csv, a.min, a.max) if a.ncu_csv else {}
     rows = []
-    if not os.environ.get("SWEEP_NCU_ONLY"):
+    if a.merge:
+        rows = json.load(open(a.merge))["rows"]
+        for row in rows:
+            m = ncu.get(row["log2n"])
+            if m and row["dir"] == -1:
+                tr = m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
+                row.update(ncu_kernel=m["kernel"][:60], ncu_dram_bytes=tr,
+                           ncu_traffic_ratio=tr / (16.0 * row["n"] * row["batch"]),
+                           ncu_ms=m.get("gpu__time_duration.sum", 0) * 1e3)
+            print(f"N=2^{row['log2n']:<2} dir={row['dir']:+d} {row['variant']:>6} {row['ms']:7.3f} ms "
+                  f"{row['alg_GBps']:7.1f} GB/s {row['frac']:6.1%}" +
+                  (f"  ncu DRAM {row['ncu_traffic_ratio']:.3f}x alg" if "ncu_traffic_ratio" in row else ""))
+    elif not os.environ.get("SWEEP_NCU_ONLY"):
         import torch
         import paper_1407_6915_b200 as bf
         from synth import gpu as sg
