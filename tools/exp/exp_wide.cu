@@ -17,14 +17,14 @@ static Cfg mk(const char* name) {
 }
 static Cfg table(int i) {
     switch (i) {
-        case 0: return mk<16, 16, 2, 32, TW_SPLIT>("c16 s2 g1 (default)");
-        case 1: return mk<16, 16, 3, 32, TW_SPLIT, 2>("c16 s3 g2");
+        case 0: return mk<16, 16, 2, 32, TW_SPLIT>("c16 s2 g1");
+        case 1: return mk<16, 16, 3, 32, TW_SPLIT, 2>("c16 s3 g2 (default)");
         case 2: return mk<8, 8, 6, 32, TW_SPLIT, 4>("c8 s6 g4");
-        case 3: return mk<8, 8, 5, 32, TW_SPLIT, 4>("c8 s5 g4");
-        case 4: return mk<8, 8, 6, 32, TW_SPLIT, 3>("c8 s6 g3");
-        case 5: return mk<8, 8, 4, 32, TW_SPLIT, 2>("c8 s4 g2");
-        case 6: return mk<8, 8, 3, 32, TW_SPLIT, 2>("c8 s3 g2");
-        case 7: return mk<16, 16, 3, 32, TW_SPLIT, 2, 2>("c16 s3 g2 cb2");
+        case 3: return mk<8, 8, 4, 32, TW_SPLIT, 3>("c8 s4 g3");
+        case 4: return mk<8, 8, 3, 32, TW_SPLIT, 2>("c8 s3 g2");
+        case 5: return mk<16, 16, 4, 32, TW_SPLIT, 3>("c16 s4 g3");
+        case 6: return mk<16, 16, 5, 32, TW_SPLIT, 4>("c16 s5 g4");
+        case 7: return mk<32, 32, 3, 32, TW_SPLIT, 2>("c32 s3 g2");
         default: return Cfg{nullptr, 0, 0, 0, 0, 0, 0, 0, 0, nullptr, 1};
     }
 }
