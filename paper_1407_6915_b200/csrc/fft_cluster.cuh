@@ -82,18 +82,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
             : "memory");
     } while (!done);
 }
-// Non-blocking: has the phase with parity `parity` completed?
-__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
-    uint32_t done = 0;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    return done != 0;
-}
 // Remote 8-byte store into another CTA's shared memory that counts 8 bytes
 // against that CTA's mbarrier `rbar` (both shared::cluster addresses).
 __device__ __forceinline__ void st_async(uint32_t raddr, float2 v, uint32_t rbar) {

@@ -552,52 +552,30 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
         }
     } else if (warp == WR) {
         // ============================================== release
-        // Task k: recycle its stage as soon as the compute warps have read it for the
-        // last time (sfree -> empty), wait until its stores are issued (done), then
-        // publish.  A fence.acq_rel.gpu takes microseconds, so every later task that
-        // is already finished (non-blocking tests, in order, at most NSTAGE ahead) is
-        // recycled and published under the same fence.
         if (lane == 0) {
-            uint32_t recycled = 0;   // tasks < recycled have had their stage recycled
-            int bkind[NSTAGE], bslot[NSTAGE];
-            for (uint32_t k = 0;;) {
+            for (uint32_t k = 0;; ++k) {
                 const uint32_t s = k % NSTAGE, u = k / NSTAGE;
                 mbar_wait(full0 + 8 * s, u & 1);
                 const PipeTask d = info[s];
                 if (d.kind == 2) break;
                 P2_T(rt0)
                 BFFT_STRESS_DELAY(11);
-                if (k >= recycled) {
-                    mbar_wait(sfree0 + 8 * s, u & 1);
-                    mbar_arrive(empty0 + 8 * s);   // stage reusable: its last exchange has been read
-                    recycled = k + 1;
-                }
+                mbar_wait(sfree0 + 8 * s, u & 1);
+                mbar_arrive(empty0 + 8 * s);   // stage reusable: its last exchange has been read
                 mbar_wait(done0 + 8 * s, u & 1);
-                int nb = 0;
-                bkind[nb] = d.kind;
-                bslot[nb++] = (int)(d.rec % S);
-                uint32_t j = k + 1;
-                for (; j < k + NSTAGE; ++j) {         // later tasks already finished join the batch
-                    const uint32_t sj = j % NSTAGE, uj = j / NSTAGE;
-                    if (!mbar_test(full0 + 8 * sj, uj & 1)) break;
-                    const PipeTask dj = info[sj];
-                    if (dj.kind == 2) break;
-                    if (j >= recycled) {
-                        if (!mbar_test(sfree0 + 8 * sj, uj & 1)) break;
-                        mbar_arrive(empty0 + 8 * sj);
-                        recycled = j + 1;
-                    }
-                    if (!mbar_test(done0 + 8 * sj, uj & 1)) break;
-                    bkind[nb] = dj.kind;
-                    bslot[nb++] = (int)(dj.rec % S);
-                }
                 P2_T(rt1)
                 BFFT_STRESS_DELAY(12);
 #ifndef BFFT_PIPE_NODEPS
-                fence_acq_rel_gpu();            // their stores, observed through done[], become visible
+#ifndef BFFT_PIPE_REDREL
+                fence_acq_rel_gpu();            // their stores, observed through done[s], become visible
 #endif
-                for (int i = 0; i < nb; ++i) red_relaxed_gpu((bkind[i] == 0 ? doneA : doneB) + bslot[i], 1);
-                k = j;
+#endif
+                const int slot = (int)(d.rec % S);
+#ifdef BFFT_PIPE_REDREL
+                red_release_gpu((d.kind == 0 ? doneA : doneB) + slot, 1);
+#else
+                red_relaxed_gpu((d.kind == 0 ? doneA : doneB) + slot, 1);
+#endif
                 P2_T(rt2)
                 P2_ACC(16, rt0, rt1)
                 P2_ACC(17, rt1, rt2)
