@@ -165,13 +165,34 @@ struct RowsMinBlocks {  // CTAs per SM the register budget is sized for
     static constexpr int V = PP == 32 ? (THREADS <= 256 ? 2 : 1) : (THREADS <= 256 ? 3 : 1);
 };
 
-template <int L, int B, bool INV, int PP = 16, int MINB = 0>   // MINB > 0 overrides the register budget
+// W_n^k of a real-record plan (n = 2L real points), fp64-computed tables:
+// W_n^k = hi[k >> lb] * lo[k & (2^lb - 1)] (csrc/real.cu's factors).
+struct RealTw {
+    const float2* hi;
+    const float2* lo;
+    int lb;
+    __device__ __forceinline__ float2 operator()(int k) const {
+        return cmul(__ldg(hi + (k >> lb)), __ldg(lo + (k & ((1 << lb) - 1))));
+    }
+};
+
+// REAL = 0: complex records.  REAL = 1: real records, forward (R2C): the
+// record is the L-point complex signal x[2m] + i x[2m+1]; after its transform
+// Z the split X[k] = E + W_n^k O (E = (Z[k] + conj Z[L-k])/2, O = (Z[k] -
+// conj Z[L-k])/(2i)) is done in the same kernel, partners read from shared
+// memory, and the packed half spectrum (out[0] = (X[0], X[L])) is stored.
+// REAL = 2: inverse (C2R): the merge Z[k] = E + i O (E = (X[k] + conj
+// X[L-k])/2, O = (X[k] - conj X[L-k]) conj(W_n^k)/2) happens on load (the
+// partner read straight from global memory), then the inverse transform.
+// csrc/real.cu holds the same arithmetic as separate kernels for longer records.
+template <int L, int B, bool INV, int PP = 16, int MINB = 0, int REAL = 0>   // MINB > 0 overrides the register budget
 __global__ void __launch_bounds__(B * Sched<L, PP>::T, MINB > 0 ? MINB : RowsMinBlocks<L, B, PP>::V)
 k_rows(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
-       const float2* __restrict__ tw, float scale, int64_t istride, const float* __restrict__ window) {
+       const float2* __restrict__ tw, float scale, int64_t istride, const float* __restrict__ window, RealTw rt) {
     // istride: elements between consecutive input records (L for records; the
     // hop for STFT frames); window: optional real
     // per-sample weights w[0..L) applied on load (STFT), nullptr = none
+    static_assert(REAL == 0 || INV == (REAL == 2), "R2C is forward, C2R inverse");
     using S = Sched<L, PP>;
     constexpr int P = S::P, T = S::T;
     extern __shared__ float2 sm[];
@@ -186,7 +207,19 @@ k_rows(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
         float2 v[P];
 #pragma unroll
         for (int s = 0; s < P; ++s) {
-            float2 x = ok ? ld_stream(src + s * T) : make_float2(0.f, 0.f);
+            // C2R reads every element twice (as itself and as a partner): keep it cached
+            float2 x = ok ? (REAL == 2 ? __ldg(src + s * T) : ld_stream(src + s * T)) : make_float2(0.f, 0.f);
+            if constexpr (REAL == 2) {
+                const int k = t + s * T;
+                if (k == 0) {
+                    x = make_float2(0.5f * (x.x + x.y), 0.5f * (x.x - x.y));      // (E[0], O[0])
+                } else {
+                    const float2 y = ok ? __ldg(in + r * istride + (L - k)) : make_float2(0.f, 0.f);
+                    const float2 e = __fmul2_rn(cadd(x, conjf2(y)), make_float2(0.5f, 0.5f));
+                    const float2 o = cmul(__fmul2_rn(csub(x, conjf2(y)), make_float2(0.5f, 0.5f)), conjf2(rt(k)));
+                    x = cadd(e, mul_pi(o));                                       // Z[k] = E + i O
+                }
+            }
             if (window) {
                 const float w = __ldg(window + t + s * T);
                 x = make_float2(x.x * w, x.y * w);
@@ -194,7 +227,30 @@ k_rows(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
             v[s] = INV ? conjf2(x) : x;
         }
         fft_engine<L, PP>(v, t, sm, addr, tab);
-        if (ok) {
+        if constexpr (REAL == 1) {
+            __syncthreads();   // every exchange of the engine has been read
+#pragma unroll
+            for (int q = 0; q < P; ++q) sm[addr(t + q * T)] = v[q];
+            __syncthreads();
+            if (ok) {
+                float2* dst = out + r * (int64_t)L + t;
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    const int k = t + q * T;
+                    const float2 a = v[q];
+                    float2 x;
+                    if (k == 0) {
+                        x = make_float2(a.x + a.y, a.x - a.y);                     // (X[0], X[L])
+                    } else {
+                        const float2 c = sm[addr(L - k)];
+                        const float2 e = __fmul2_rn(cadd(a, conjf2(c)), make_float2(0.5f, 0.5f));
+                        const float2 o = mul_mi(__fmul2_rn(csub(a, conjf2(c)), make_float2(0.5f, 0.5f)));
+                        x = cadd(e, cmul(o, rt(k)));                               // X[k] = E + W^k O
+                    }
+                    st_stream(dst + q * T, x);
+                }
+            }
+        } else if (ok) {
             float2* dst = out + r * (int64_t)L + t;
 #pragma unroll
             for (int q = 0; q < P; ++q) st_stream(dst + q * T, INV ? scale_conj(v[q], scale) : v[q]);

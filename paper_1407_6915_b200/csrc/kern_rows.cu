@@ -18,6 +18,16 @@ template <int L> struct FsGeom {
 };
 
 
+template <int L, int PP = 16, int MINB = 0> static KernelSet row_real_kernel(bool inv) {
+    using G = RowGeom<L, PP>;
+    KernelSet k;
+    k.fn = inv ? (const void*)&k_rows<L, G::B, true, PP, MINB, 2> : (const void*)&k_rows<L, G::B, false, PP, MINB, 1>;
+    k.threads = G::THREADS;
+    k.smem = sizeof(float2) * RowLayout::size(G::B * L);   // the partner exchange needs shared memory at any L
+    k.cols = G::B;
+    k.pp = PP;
+    return k;
+}
 template <int L, int PP = 16, int MINB = 0> static KernelSet row_kernel(bool inv) {
     using G = RowGeom<L, PP>;
     KernelSet k;
@@ -61,6 +71,16 @@ KernelSet pick_row(int log2l, bool inv) {
         // radix-32 engines at 2^13 and 2^14 (profiles/r01_rows_2p13_minb.txt)
         case 13: return row_kernel<8192, 32>(inv);
         case 14: return row_kernel<16384, 32>(inv);
+        default: return KernelSet{};
+    }
+}
+KernelSet pick_row_real(int log2l, bool inv) {
+    switch (log2l) {
+#define M(k, L) case k: return row_real_kernel<L>(inv);
+        BFFT_L_CASES(M)
+#undef M
+        case 12: return row_real_kernel<4096>(inv);
+        case 13: return row_real_kernel<8192, 32>(inv);
         default: return KernelSet{};
     }
 }

@@ -461,9 +461,10 @@ extern "C" fft_plan* fft_plan_create_real(int64_t n, int64_t batch, int dir) {
     p->device = p->inner->device;
     p->sms = p->inner->sms;
     p->variant = p->inner->variant;
-    // W_n^k for k <= n/4 as hi[k >> lb] * lo[k & (2^lb - 1)], fp64 -> fp32 (reading c9)
+    // W_n^k for k <= n/2 as hi[k >> lb] * lo[k & (2^lb - 1)], fp64 -> fp32 (reading c9)
     p->rt_lb = p->log2n / 2;
-    const int64_t nhi = ((n / 4) >> p->rt_lb) + 1, nlo = 1ll << p->rt_lb;
+    // k up to n/2: the fused single-pass kernel evaluates X[k] for every k < n/2
+    const int64_t nhi = ((n / 2) >> p->rt_lb) + 1, nlo = 1ll << p->rt_lb;
     std::vector<float2> t;
     for (int64_t a = 0; a < nhi; ++a) {
         const double ang = -2.0 * M_PI * (double)(a << p->rt_lb) / (double)n;
@@ -486,6 +487,22 @@ extern "C" fft_plan* fft_plan_create_real(int64_t n, int64_t batch, int dir) {
     }
     p->tw_a = p->d_tab;
     p->tw_b = p->d_tab + nhi;
+    if (p->inner->variant == FFT_VARIANT_SINGLE) {
+        // records of up to 2^14 reals: one kernel, the split / merge fused into the
+        // single-pass transform (k_rows<..., REAL>); longer records: two kernels
+        p->ka = pick_row_real(ilog2((int)(n / 2)), dir == FFT_INVERSE);
+        if (!p->ka.fn) {
+            bfft_set_error(FFT_E_SIZE, "unsupported transform size: %lld", (long long)n);
+            return fail();
+        }
+        if (set_smem(p->ka)) return fail();
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ_a, p->ka.fn, p->ka.threads, p->ka.smem);
+        if (e != cudaSuccess) {
+            bfft_set_error(FFT_E_CUDA, "occupancy query failed: %s", cudaGetErrorString(e));
+            return fail();
+        }
+        p->occ_a = std::max(p->occ_a, 1);
+    }
     return p;
 }
 
@@ -538,7 +555,7 @@ extern "C" int fft_plan_get_info(const fft_plan* p, fft_plan_info* info) {
         int rc = fft_plan_get_info(p->inner, info);
         info->n = p->n;
         info->dir = p->dir;
-        info->kernels_per_exec += 1;                 // + the split / merge kernel
+        if (!p->ka.fn) info->kernels_per_exec += 1;  // + the split / merge kernel (fused up to 2^14)
         info->table_bytes += (int64_t)p->tab_bytes;
         info->real = 1;
         info->hop = 0;
@@ -591,7 +608,8 @@ static int launch(const fft_plan* p, const float2* in, float2* out, int64_t coun
             const int64_t groups = (count + p->ka.cols - 1) / p->ka.cols;
             const int grid = (int)std::min<int64_t>(groups, (int64_t)p->sms * p->occ_a * 8);
             auto fn = (RowFn)p->ka.fn;
-            fn<<<grid, p->ka.threads, p->ka.smem, st>>>(in, out, count, p->tw_a, p->scale, istride, window);
+            fn<<<grid, p->ka.threads, p->ka.smem, st>>>(in, out, count, p->tw_a, p->scale, istride, window,
+                                                         RealTw{nullptr, nullptr, 0});
             break;
         }
         case FFT_VARIANT_CLUSTER: {
@@ -697,6 +715,16 @@ extern "C" int fft_exec_range(const fft_plan* p, const void* in, void* out, int6
         // inverse = the merge into `out`, then the complex inverse in place
         const int64_t h = p->n / 2;
         cudaStream_t st = (cudaStream_t)stream;
+        if (p->ka.fn) {   // fused single-pass kernel
+            const int64_t groups = (count + p->ka.cols - 1) / p->ka.cols;
+            const int grid = (int)std::min<int64_t>(groups, (int64_t)p->sms * p->occ_a * 8);
+            ((RowFn)p->ka.fn)<<<grid, p->ka.threads, p->ka.smem, st>>>(
+                (const float2*)in, (float2*)out, count, p->inner->tw_a, p->inner->scale, h, nullptr,
+                RealTw{p->tw_a, p->tw_b, p->rt_lb});
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return bfft_set_error(FFT_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+            return FFT_OK;
+        }
         if (p->dir == FFT_FORWARD) {
             int rc = launch(p->inner, (const float2*)in, (float2*)out, count, st);
             if (rc) return rc;

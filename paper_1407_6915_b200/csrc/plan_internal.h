@@ -6,6 +6,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+namespace bfft {
+struct RealTw;   // fft_kernels.cuh
+}
+
 struct KernelSet {
     const void* fn = nullptr;
     int threads = 0;
@@ -26,7 +30,7 @@ struct ClusterChoice {
 };
 
 // kernel signatures, by family (launch casts KernelSet::fn to these)
-using RowFn = void (*)(const float2*, float2*, int64_t, const float2*, float, int64_t, const float*);
+using RowFn = void (*)(const float2*, float2*, int64_t, const float2*, float, int64_t, const float*, bfft::RealTw);
 using ColFn = void (*)(const float2*, float2*, int64_t, int, const float2*);
 using RowTFn = void (*)(const float2*, float2*, int64_t, int, const float2*, float);
 using ClusterFn = void (*)(const CUtensorMap, float2*, int64_t, const float2*, const float2*, float);
@@ -40,6 +44,9 @@ using Pipe2Fn = void (*)(const CUtensorMap, float2*, float2*, int64_t, int*, int
 
 // kern_rows.cu: single-pass row kernel for 2^log2l; four-step column / row kernels
 KernelSet pick_row(int log2l, bool inv);
+// kern_rows.cu: the single-pass kernel with the real-record split (R2C, !inv)
+// or merge (C2R, inv) fused, for real records of n = 2^(log2l+1) points
+KernelSet pick_row_real(int log2l, bool inv);
 KernelSet pick_fs_col(int log2l, int n2, bool inv);
 KernelSet pick_fs_row(int log2l, bool inv);
 // kern_cluster.cu: cluster kernel for 2^log2n (want_c = requested cluster size or 0)
