@@ -240,6 +240,21 @@ template <int COLS>
 struct ColLayout {
     __device__ __forceinline__ static int at(int e, int c) { return e * COLS + c; }
 };
+// Column layout for tiles narrower than 16 columns: one pad slot of COLS
+// entries per R0 elements (R0 = the schedule's first radix).  The first
+// Stockham pass writes element 16t + q-like runs whose plain addresses fall on
+// the same bank pair for every t of a warp (2-4x the minimum wavefronts at
+// COLS = 8 / 4, ncu: mio-bound at 2^21 / 2^22); the pad spreads them
+// (tools/bank_model.py: every pass at the minimum).  COLS >= 16: plain.
+template <int COLS, int R0>
+struct PadColLayout {
+    static constexpr int SH = ilog2(R0);
+    __device__ __forceinline__ static int at(int e, int c) {
+        if constexpr (COLS >= 16) return e * COLS + c;
+        else return e * COLS + c + COLS * (e >> SH);
+    }
+    __host__ __device__ static constexpr int size(int L) { return COLS >= 16 ? COLS * L : COLS * (L + (L >> SH)); }
+};
 // Swizzled column layout for transposing accesses (a half-warp on 16
 // consecutive elements e of one column): c ^ (e mod COLS) spreads them over
 // 16 distinct bank pairs.

@@ -357,9 +357,13 @@ struct Pipe2Cfg {
     static constexpr int NT = NTC * NGRP + 64;                   // + producer warp + release warp
     static constexpr int TA = N2 / COLS, TB = N1 / ROWS;
     static constexpr int RSTRIDE = N2 + 2;                       // padded B-tile row (16-B multiple)
-    static constexpr int TILE_A = COLS * N1, TILE_B = ROWS * RSTRIDE;
+    using LayA = PadColLayout<COLS, Sched<N1, PP>::R0>;           // exchange layouts (fft_device.cuh)
+    using LayB = PadColLayout<ROWS, Sched<N2, PP>::R0>;
+    static constexpr int TILE_A0 = LayA::size(N1) > COLS * N1 ? LayA::size(N1) : COLS * N1;
+    static constexpr int TILE_B0 = ROWS * RSTRIDE > LayB::size(N2) ? ROWS * RSTRIDE : LayB::size(N2);
+    static constexpr int TILE_A = COLS * N1, TILE_B = ROWS * RSTRIDE;   // bytes the copies bring
     // stage stride rounded to 128 bytes: TMA writes shared memory at 128-byte aligned addresses
-    static constexpr int TILE = ((TILE_A > TILE_B ? TILE_A : TILE_B) + 15) / 16 * 16;
+    static constexpr int TILE = ((TILE_A0 > TILE_B0 ? TILE_A0 : TILE_B0) + 15) / 16 * 16;
     static constexpr int BOXR = N1 < 256 ? N1 : 256;             // TMA box rows
     static constexpr int TB2 = Sched<N2, PP>::T;
     // split four-step twiddles (TW_SPLIT): B-side tables in shared memory,
@@ -628,7 +632,7 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                     v[q] = INV ? conjf2(x) : x;
                 }
 #ifndef BFFT_PIPE_NOCOMPUTE  // (experiments only: data movement without the FFT)
-                fft_engine<N1, PP>(v, t, stage, [&](int e) { return ColLayout<COLS>::at(e, col); }, tabA, bar);
+                fft_engine<N1, PP>(v, t, stage, [&](int e) { return CF::LayA::at(e, col); }, tabA, bar);
 #endif
 #ifndef BFFT_PIPE_NOFENCE
                 fence_proxy_async_smem();   // last generic access of the stage: before its next TMA refill
@@ -689,7 +693,7 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                     for (int q = 0; q < PP; ++q) v[q] = stage[col * RSTRIDE + t + q * TB2];
                 }
 #ifndef BFFT_PIPE_NOCOMPUTE
-                fft_engine<N2, PP>(v, t, stage, [&](int e) { return ColLayout<ROWS>::at(e, col); }, tabB, bar);
+                fft_engine<N2, PP>(v, t, stage, [&](int e) { return CF::LayB::at(e, col); }, tabB, bar);
 #endif
 #ifndef BFFT_PIPE_NOFENCE
                 fence_proxy_async_smem();   // last generic access of the stage: before its next bulk refill
