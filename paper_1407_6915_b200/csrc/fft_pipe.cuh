@@ -346,22 +346,26 @@ __device__ __forceinline__ void red_relaxed_gpu(int* p, int v) {
     asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP = 16, int NGRP = 1>
+template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP = 16, int NGRP = 1, int H = 1>
 struct Pipe2Cfg {
     static constexpr int N = N1 * N2;
     static constexpr int NTC = COLS * Sched<N1, PP>::T;        // compute threads per group
     static_assert(ROWS * Sched<N2, PP>::T == NTC, "A and B tasks use the same compute warps");
     static_assert(Sched<N1, PP>::P == PP && Sched<N2, PP>::P == PP, "N1, N2 >= PP");
     static_assert(NTC % 32 == 0, "whole compute warps");
-    static_assert(NGRP >= 1 && NGRP <= NSTAGE, "every group's end marker needs a stage of its own");
+    static_assert(NGRP >= 1 && NGRP % H == 0 && NGRP / H <= NSTAGE,
+                  "every group sequence's end marker needs a stage of its own");
+    static constexpr int NSEQ = NGRP / H;                        // task sequences (H groups share a task)
     static constexpr int NT = NTC * NGRP + 64;                   // + producer warp + release warp
-    static constexpr int TA = N2 / COLS, TB = N1 / ROWS;
+    static constexpr int TA = N2 / (H * COLS), TB = N1 / (H * ROWS);   // tasks per record
     static constexpr int RSTRIDE = N2 + 2;                       // padded B-tile row (16-B multiple)
     using LayA = PadColLayout<COLS, Sched<N1, PP>::R0>;           // exchange layouts (fft_device.cuh)
     using LayB = PadColLayout<ROWS, Sched<N2, PP>::R0>;
-    static constexpr int TILE_A0 = LayA::size(N1) > COLS * N1 ? LayA::size(N1) : COLS * N1;
-    static constexpr int TILE_B0 = ROWS * RSTRIDE > LayB::size(N2) ? ROWS * RSTRIDE : LayB::size(N2);
-    static constexpr int TILE_A = COLS * N1, TILE_B = ROWS * RSTRIDE;   // bytes the copies bring
+    // a task's H halves exchange in disjoint regions of its stage (16-entry aligned)
+    static constexpr int REG_A = (LayA::size(N1) + 15) / 16 * 16, REG_B = (LayB::size(N2) + 15) / 16 * 16;
+    static constexpr int TILE_A0 = H * REG_A > H * COLS * N1 ? H * REG_A : H * COLS * N1;
+    static constexpr int TILE_B0 = H * ROWS * RSTRIDE > H * REG_B ? H * ROWS * RSTRIDE : H * REG_B;
+    static constexpr int TILE_A = H * COLS * N1, TILE_B = H * ROWS * RSTRIDE;   // entries the copies bring
     // stage stride rounded to 128 bytes: TMA writes shared memory at 128-byte aligned addresses
     static constexpr int TILE = ((TILE_A0 > TILE_B0 ? TILE_A0 : TILE_B0) + 15) / 16 * 16;
     static constexpr int BOXR = N1 < 256 ? N1 : 256;             // TMA box rows
@@ -386,9 +390,9 @@ struct Pipe2Cfg {
 //              W_{N2 PP}^{t' q} * W_{PP^2}^{q s} from two small shared-memory
 //              tables — no global load on either task's critical path.
 enum { TW_TREE = 0, TW_TABLE = 1, TW_SPLIT = 2 };
-template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP, int TWM, int NGRP = 1>
+template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP, int TWM, int NGRP = 1, int H = 1>
 constexpr size_t pipe2_smem() {
-    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP>;
+    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP, H>;
     return CF::SMEM + (TWM == TW_SPLIT ? CF::SMEM_TW : 0);
 }
 
@@ -402,14 +406,18 @@ struct PipeTask {
 // k = g, g + NGRP, ... of the CTA's claimed sequence, each computing in the
 // stage its task was loaded into: NGRP tasks compute concurrently per CTA
 // while the producer stages the next (NSTAGE >= NGRP + 1 to overlap).
+// With H > 1 a task is H adjacent tiles (an A-task H*COLS columns — one
+// H*COLS*8-byte DRAM run per row; a B-task H*ROWS ring rows) staged together
+// and computed by H groups, one tile each: groups g = H j .. H j + H - 1 take
+// tasks k = j, j + NGRP / H, ...
 template <int N1, int N2, int COLS, int ROWS, bool INV, int NSTAGE, int PP = 16, int TWM = TW_TREE, int NGRP = 1,
-          int CB = 1, bool PF = false>
-__global__ void __launch_bounds__(Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP>::NT,
-                                  Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP>::MINB)
+          int CB = 1, bool PF = false, int H = 1>
+__global__ void __launch_bounds__(Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP, H>::NT,
+                                  Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP, H>::MINB)
 k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, float2* __restrict__ ring,
         int64_t nrec, int* __restrict__ ctr, int S, int LAG, float scale, const float2* __restrict__ w_hi,
         const float2* __restrict__ w_lo, int w_lb) {
-    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP>;
+    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP, H>;
     constexpr int LPP = ilog2(PP);
     constexpr int N = CF::N, TA = CF::TA, TB = CF::TB, NTC = CF::NTC, TILE = CF::TILE, RSTRIDE = CF::RSTRIDE;
     constexpr int TA1 = Sched<N1, PP>::T, TB2 = Sched<N2, PP>::T;
@@ -429,8 +437,8 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
         for (int i = 0; i < NSTAGE; ++i) {
             mbar_init(full0 + 8 * i, 1);
             mbar_init(empty0 + 8 * i, 1);       // the release warp frees a stage
-            mbar_init(done0 + 8 * i, NTC / 32); // one arrival per compute warp: stores issued
-            mbar_init(sfree0 + 8 * i, NTC / 32);// one arrival per compute warp: stage read for the last time
+            mbar_init(done0 + 8 * i, H * NTC / 32); // one arrival per compute warp: stores issued
+            mbar_init(sfree0 + 8 * i, H * NTC / 32);// one arrival per compute warp: stage read for the last time
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -492,7 +500,7 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                     if (valid && d.kind != 2 && decode(base + sub, nx) && nx.kind == 0) {
 #pragma unroll 1
                         for (int r0 = 0; r0 < N1; r0 += CF::BOXR)
-                            tma_prefetch_3d(&tmap_in, nx.tile * COLS, r0, (int)nx.rec);
+                            tma_prefetch_3d(&tmap_in, nx.tile * H * COLS, r0, (int)nx.rec);
                     }
                 }
             }
@@ -529,11 +537,11 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                     }
 #endif
                     info[s] = d;
-                    mbar_expect_tx(fb, (uint32_t)((d.kind == 0 ? CF::TILE_A : ROWS * N2) * sizeof(float2)));
+                    mbar_expect_tx(fb, (uint32_t)((d.kind == 0 ? CF::TILE_A : H * ROWS * N2) * sizeof(float2)));
                 }
             }
             if (d.kind == 2) {
-                if (++ends == NGRP) break;
+                if (++ends == CF::NSEQ) break;
                 ++k;
                 continue;
             }
@@ -543,13 +551,13 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 if (lane == 0) {
 #pragma unroll 1
                     for (int r0 = 0; r0 < N1; r0 += CF::BOXR)
-                        tma_load_3d_hint(smem_addr(stage + r0 * COLS), &tmap_in, d.tile * COLS, r0, (int)d.rec, fb,
-                                         pol_stream);
+                        tma_load_3d_hint(smem_addr(stage + r0 * H * COLS), &tmap_in, d.tile * H * COLS, r0,
+                                         (int)d.rec, fb, pol_stream);
                 }
             } else {
                 const int slot = (int)(d.rec % S);
-                const float2* src = ring + (int64_t)slot * N + (int64_t)d.tile * ROWS * N2;
-                for (int j = lane; j < ROWS; j += 32)
+                const float2* src = ring + (int64_t)slot * N + (int64_t)d.tile * H * ROWS * N2;
+                for (int j = lane; j < H * ROWS; j += 32)
                     bulk_g2s(smem_addr(stage + j * RSTRIDE), src + (int64_t)j * N2, N2 * sizeof(float2), fb);
             }
             ++k;
@@ -593,6 +601,8 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
         const int grp = warp / (NTC / 32);
         const int gtid = tid - grp * NTC;   // thread index within the group
         const NamedBarrier bar{1 + grp, NTC};
+        const int half = grp % H;           // which of its task's H tiles the group computes
+        const NamedBarrier pair{2 + NGRP + grp / H, H * NTC};   // the task's H groups: inputs read
         float2* tw_t = reinterpret_cast<float2*>(reinterpret_cast<char*>(sm) + CF::OFF_TW);   // T[q][s]
         float2* tw_b0 = tw_t + CF::TW_T;                                                       // WB0[t][q]
         if constexpr (TWM == TW_SPLIT) {
@@ -602,7 +612,7 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
             const NamedBarrier all{1 + NGRP, NGRP * NTC};
             all();
         }
-        for (uint32_t k = grp;; k += NGRP) {
+        for (uint32_t k = grp / H;; k += CF::NSEQ) {
             const uint32_t s = k % NSTAGE, u = k / NSTAGE;
             P2_T(ct0)
             mbar_wait(full0 + 8 * s, u & 1);
@@ -617,7 +627,7 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
             if (d.kind == 0) {
                 // ---------------- A: columns n2 of record r, FFT over n1, twiddle, -> ring
                 const int col = gtid % COLS, t = gtid / COLS;
-                const int n2 = d.tile * COLS + col;
+                const int n2 = (d.tile * H + half) * COLS + col;
                 float2 f[LPP], w0;
                 if constexpr (TWM == TW_TREE) {
 #pragma unroll
@@ -628,11 +638,13 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 }
 #pragma unroll
                 for (int q = 0; q < PP; ++q) {
-                    const float2 x = stage[(t + q * TA1) * COLS + col];
+                    const float2 x = stage[(t + q * TA1) * (H * COLS) + half * COLS + col];
                     v[q] = INV ? conjf2(x) : x;
                 }
+                if constexpr (H > 1) pair();   // the halves' exchange regions overlap both halves' inputs
+                float2* xch = stage + half * CF::REG_A;
 #ifndef BFFT_PIPE_NOCOMPUTE  // (experiments only: data movement without the FFT)
-                fft_engine<N1, PP>(v, t, stage, [&](int e) { return CF::LayA::at(e, col); }, tabA, bar);
+                fft_engine<N1, PP>(v, t, xch, [&](int e) { return CF::LayA::at(e, col); }, tabA, bar);
 #endif
 #ifndef BFFT_PIPE_NOFENCE
                 fence_proxy_async_smem();   // last generic access of the stage: before its next TMA refill
@@ -669,7 +681,8 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
             } else {
                 // ---------------- B: rows k1 of record r, FFT over n2, -> X[k1 + N1 k2]
                 const int col = gtid % ROWS, t = gtid / ROWS;
-                const int k0 = d.tile * ROWS;
+                const int k0 = (d.tile * H + half) * ROWS;
+                const float2* srow = stage + (half * ROWS + col) * RSTRIDE;
                 {   // the tile's ring rows are staged: drop them from L2 (no write-back)
                     const char* rows = reinterpret_cast<const char*>(ring + (int64_t)slot * N + (int64_t)k0 * N2);
                     for (int i = gtid; i < ROWS * N2 * 8 / 128; i += NTC) l2_discard128(rows + 128 * i);
@@ -685,15 +698,17 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                     for (int q0 = 0; q0 < PP; q0 += 8) {
 #pragma unroll
                         for (int q = q0; q < q0 + 8; ++q)
-                            v[q] = cmul(stage[col * RSTRIDE + t + q * TB2], cmul(wb, trow[q]));
+                            v[q] = cmul(srow[t + q * TB2], cmul(wb, trow[q]));
                         asm volatile("" ::: "memory");
                     }
                 } else {
 #pragma unroll
-                    for (int q = 0; q < PP; ++q) v[q] = stage[col * RSTRIDE + t + q * TB2];
+                    for (int q = 0; q < PP; ++q) v[q] = srow[t + q * TB2];
                 }
+                if constexpr (H > 1) pair();
+                float2* xch = stage + half * CF::REG_B;
 #ifndef BFFT_PIPE_NOCOMPUTE
-                fft_engine<N2, PP>(v, t, stage, [&](int e) { return CF::LayB::at(e, col); }, tabB, bar);
+                fft_engine<N2, PP>(v, t, xch, [&](int e) { return CF::LayB::at(e, col); }, tabB, bar);
 #endif
 #ifndef BFFT_PIPE_NOFENCE
                 fence_proxy_async_smem();   // last generic access of the stage: before its next bulk refill

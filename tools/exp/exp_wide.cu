@@ -7,13 +7,14 @@
 #include <vector>
 using namespace bfft;
 
-struct Cfg { const void* fn; int threads; size_t smem; int cols, rows, stages, twm, boxr, pp; const char* name; int cb; };
+struct Cfg { const void* fn; int threads; size_t smem; int cols, rows, stages, twm, boxr, pp; const char* name; int cb; int h; };
 
-template <int COLS, int ROWS, int NST, int PP, int TWM, int NGRP = 1, int CB = 1, bool PF = false>
+template <int COLS, int ROWS, int NST, int PP, int TWM, int NGRP = 1, int CB = 1, bool PF = false, int H = 1>
 static Cfg mk(const char* name) {
-    using CF = Pipe2Cfg<256, 256, COLS, ROWS, NST, PP, NGRP>;
-    return Cfg{(const void*)&k_pipe2<256, 256, COLS, ROWS, false, NST, PP, TWM, NGRP, CB, PF>, CF::NT,
-               pipe2_smem<256, 256, COLS, ROWS, NST, PP, TWM, NGRP>(), COLS, ROWS, NST, TWM, CF::BOXR, PP, name, CB};
+    using CF = Pipe2Cfg<256, 256, COLS, ROWS, NST, PP, NGRP, H>;
+    return Cfg{(const void*)&k_pipe2<256, 256, COLS, ROWS, false, NST, PP, TWM, NGRP, CB, PF, H>, CF::NT,
+               pipe2_smem<256, 256, COLS, ROWS, NST, PP, TWM, NGRP, H>(), COLS, ROWS, NST, TWM, CF::BOXR, PP, name, CB,
+               H};
 }
 static Cfg table(int i) {
     switch (i) {
@@ -25,10 +26,16 @@ static Cfg table(int i) {
         case 5: return mk<16, 16, 4, 32, TW_SPLIT, 3>("c16 s4 g3");
         case 6: return mk<16, 16, 5, 32, TW_SPLIT, 4>("c16 s5 g4");
         case 7: return mk<32, 32, 3, 32, TW_SPLIT, 2>("c32 s3 g2");
-        default: return Cfg{nullptr, 0, 0, 0, 0, 0, 0, 0, 0, nullptr, 1};
+        case 8: return mk<16, 16, 3, 32, TW_SPLIT, 4, 1, false, 2>("c16 h2 s3 g4");
+        case 9: return mk<16, 16, 3, 32, TW_SPLIT, 4, 2, false, 2>("c16 h2 s3 g4 cb2");
+        case 10: return mk<16, 16, 2, 32, TW_SPLIT, 2, 1, false, 2>("c16 h2 s2 g2");
+        case 11: return mk<16, 16, 4, 32, TW_SPLIT, 4, 1, false, 2>("c16 h2 s4 g4");
+        case 12: return mk<8, 8, 3, 32, TW_SPLIT, 4, 1, false, 2>("c8 h2 s3 g4");
+        case 13: return mk<8, 8, 3, 32, TW_SPLIT, 8, 1, false, 4>("c8 h4 s3 g8");
+        default: return Cfg{nullptr, 0, 0, 0, 0, 0, 0, 0, 0, nullptr, 1, 1};
     }
 }
-extern "C" int exp_ncfg() { return 8; }
+extern "C" int exp_ncfg() { return 14; }
 // the constant-memory Stockham twiddles of this translation unit (same table as plan.cu builds)
 static void stockham_table(int L, std::vector<float2>& out, int P) {
     out.clear();
@@ -68,7 +75,7 @@ extern "C" float exp_run(int i, const void* in, void* out, void* ring, int* ctr,
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, c.fn, c.threads, c.smem);
     if (occ < 1) return -2.f;
-    const int resident = occ * 148, per_round = 256 / c.cols + 256 / c.rows;
+    const int resident = occ * 148, per_round = 256 / (c.cols * c.h) + 256 / (c.rows * c.h);
     const long long inflight = (long long)resident * (c.stages + c.cb);
     const long long rounds = (inflight + per_round - 1) / per_round;
     int LAG = (int)(3 * rounds / 2 + 1);
@@ -81,7 +88,7 @@ extern "C" float exp_run(int i, const void* in, void* out, void* ring, int* ctr,
     CUtensorMap tm;
     cuuint64_t dims[3] = {256, 256, (cuuint64_t)nrec};
     cuuint64_t strides[2] = {256 * 8, 65536 * 8};
-    cuuint32_t box[3] = {(cuuint32_t)c.cols, (cuuint32_t)c.boxr, 1}, es[3] = {1, 1, 1};
+    cuuint32_t box[3] = {(cuuint32_t)(c.cols * c.h), (cuuint32_t)c.boxr, 1}, es[3] = {1, 1, 1};
     enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(in), dims, strides, box, es,
         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
