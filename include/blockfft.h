@@ -101,6 +101,8 @@ fft_plan *fft_plan_create_ex(int64_t n, int64_t batch, int dir, int variant);
 typedef struct fft_plan_opts {
     int variant;      /* enum fft_variant (0 = auto)                          */
     int impl;         /* implementation inside the variant, 0 = default:
+                         FFT_VARIANT_SINGLE  1 k_rows, 2 k_rows_tma (2^13;
+                                             records staged by TMA);
                          FFT_VARIANT_PIPE    1 k_pipe, 2 k_pipe2, 3 k_pipe3;
                          FFT_VARIANT_CLUSTER 1 k_cluster1 (single buffer),
                                              2 k_cluster2 (pipelined),

@@ -1,6 +1,7 @@
 // kern_rows.cu — single-pass row kernels (k_rows) and the two-kernel four-step (k_fs_cols, k_fs_rows): instantiations and pickers, compiled as its own translation unit
 // (kernel instantiations dominate build time; plan.cu only dispatches).
 #include "fft_kernels.cuh"
+#include "fft_rows_tma.cuh"
 #include "plan_internal.h"
 
 using namespace bfft;
@@ -71,6 +72,25 @@ KernelSet pick_row(int log2l, bool inv) {
         // radix-32 engines at 2^13 and 2^14 (profiles/r01_rows_2p13_minb.txt)
         case 13: return row_kernel<8192, 32>(inv);
         case 14: return row_kernel<16384, 32>(inv);
+        default: return KernelSet{};
+    }
+}
+// k_rows_tma (fft_rows_tma.cuh): records streamed into shared-memory stages by a
+// producer warp; two compute groups over three 68 KiB stages at 2^13 (79.8 %
+// vs k_rows 73.9 %; 2^12 and shorter gain nothing: profiles/r02_rows_tma.txt)
+template <int L, int PP, int NGRP, int NSTAGE> static KernelSet row_tma_kernel(bool inv) {
+    using CF = RowsTmaCfg<L, PP, NGRP, NSTAGE>;
+    KernelSet k;
+    k.fn = inv ? (const void*)&k_rows_tma<L, true, PP, NGRP, NSTAGE> : (const void*)&k_rows_tma<L, false, PP, NGRP, NSTAGE>;
+    k.threads = CF::NT;
+    k.smem = CF::SMEM;
+    k.cols = 1;
+    k.pp = PP;
+    return k;
+}
+KernelSet pick_row_tma(int log2l, bool inv) {
+    switch (log2l) {
+        case 13: return row_tma_kernel<8192, 32, 2, 3>(inv);
         default: return KernelSet{};
     }
 }

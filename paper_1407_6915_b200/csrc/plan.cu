@@ -161,6 +161,9 @@ struct fft_plan {
     float2* d_scratch = nullptr;      // four-step wave scratch
     int64_t wave = 0;                 // records per four-step wave
     KernelSet ka, kb;                 // kernels (kb only for four-step)
+    KernelSet kt;                     // single pass: k_rows_tma for contiguous records (ka = k_rows
+                                      // stays for strided / windowed STFT frames)
+    int occ_t = 0;
     int grid_a = 0, grid_b = 0;       // persistent/capped grid sizes (per full batch)
     int occ_a = 0, occ_b = 0;
     int real = 0;                     // 1: real records (fft_plan_create_real), n reals each
@@ -218,6 +221,11 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, const fft_p
     } else if (variant == FFT_VARIANT_SINGLE) {
         if (p->log2n > 14) return bfft_set_error(FFT_E_SIZE, "unsupported transform size for single-pass variant: %lld", (long long)n);
         p->ka = pick_row(p->log2n, inv);
+        if (o.impl > 2) return bfft_set_error(FFT_E_ARG, "single-pass impl must be 0, 1 (k_rows) or 2 (k_rows_tma): %d", o.impl);
+        if (o.impl != 1) p->kt = pick_row_tma(p->log2n, inv);
+        if (o.impl == 2 && !p->kt.fn)
+            return bfft_set_error(FFT_E_SIZE, "no k_rows_tma kernel for n = %lld", (long long)n);
+        if (p->kt.fn && p->kt.pp != p->ka.pp) p->kt = KernelSet{};   // they share the plan's twiddle table
         p->n1 = (int)n;
         p->n2 = 1;
         stockham_table((int)n, ta, p->ka.pp);
@@ -305,6 +313,12 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, const fft_p
         if (rc) return rc;
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ_a, p->ka.fn, p->ka.threads, p->ka.smem));
         p->occ_a = std::max(p->occ_a, 1);
+        if (p->kt.fn) {
+            rc = set_smem(p->kt);
+            if (rc) return rc;
+            CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ_t, p->kt.fn, p->kt.threads, p->kt.smem));
+            if (p->occ_t < 1) return bfft_set_error(FFT_E_CUDA, "k_rows_tma cannot be scheduled (%zu B shared memory)", p->kt.smem);
+        }
     } else if (variant == FFT_VARIANT_CLUSTER) {
         rc = set_smem(p->ka);
         if (rc) return rc;
@@ -605,6 +619,13 @@ static int launch(const fft_plan* p, const float2* in, float2* out, int64_t coun
             break;
         }
         case FFT_VARIANT_SINGLE: {
+            if (p->kt.fn && istride == n && !window) {
+                // contiguous records: persistent staged kernel, one CTA per SM slot
+                const int grid = (int)std::min<int64_t>(count, (int64_t)p->sms * p->occ_t);
+                if (grid > 0)
+                    ((RowTmaFn)p->kt.fn)<<<grid, p->kt.threads, p->kt.smem, st>>>(in, out, count, p->tw_a, p->scale);
+                break;
+            }
             const int64_t groups = (count + p->ka.cols - 1) / p->ka.cols;
             const int grid = (int)std::min<int64_t>(groups, (int64_t)p->sms * p->occ_a * 8);
             auto fn = (RowFn)p->ka.fn;

@@ -145,7 +145,7 @@ def test_closed_forms_on_gpu(variant, n):
     assert np.all(y[4] == 0)                                           # zeros stay exactly zero
 
 
-@pytest.mark.parametrize("variant,n", [(1, 256), (1, 4096), (2, 1 << 16), (2, 1 << 17), (3, 1 << 20), (5, 1 << 16),
+@pytest.mark.parametrize("variant,n", [(1, 256), (1, 4096), (1, 8192), (2, 1 << 16), (2, 1 << 17), (3, 1 << 20), (5, 1 << 16),
                                        (5, 1 << 20)])
 def test_batch_position_bit_identity(variant, n):
     # a record's result does not depend on the batch around it
@@ -237,6 +237,30 @@ def test_cluster_sizes(cs, n):
     y, info = gpu_run(x, bf.FFT_FORWARD, bf.VARIANT_CLUSTER, cluster_size=cs)
     assert info["cluster"] == cs
     check(x, bf.FFT_FORWARD, bf.VARIANT_CLUSTER, cluster_size=cs)
+
+
+@pytest.mark.parametrize("impl", [1, 2])
+@pytest.mark.parametrize("b", [1, 3, 449])
+def test_single_implementations(impl, b):
+    # 2^13: k_rows (impl 1) and k_rows_tma (impl 2, the default: records staged by
+    # bulk copies, two compute groups over three stages); 449 records = three or
+    # more per persistent CTA, so every stage and both groups are reused
+    n = 1 << 13
+    x = synth.random_records(61 + impl + b, n, 0, b)
+    check(x, bf.FFT_FORWARD, bf.VARIANT_SINGLE, impl=impl)
+    check(x, bf.FFT_INVERSE, bf.VARIANT_SINGLE, impl=impl)
+    y_out, _ = gpu_run(x, bf.FFT_FORWARD, bf.VARIANT_SINGLE, impl=impl)
+    y_in, _ = gpu_run(x, bf.FFT_FORWARD, bf.VARIANT_SINGLE, inplace=True, impl=impl)
+    assert np.array_equal(y_in, y_out)
+
+
+def test_single_impl_rejected():
+    with pytest.raises(bf.FFTError) as ei:
+        bf.Plan(4096, 1, bf.FFT_FORWARD, bf.VARIANT_SINGLE, impl=2)   # k_rows_tma only at 2^13
+    assert ei.value.code == 1
+    with pytest.raises(bf.FFTError) as ei:
+        bf.Plan(8192, 1, bf.FFT_FORWARD, bf.VARIANT_SINGLE, impl=3)
+    assert ei.value.code == 4
 
 
 @pytest.mark.parametrize("impl,n", [(1, 1 << 13), (1, 1 << 16), (1, 1 << 20), (1, 1 << 21), (1, 1 << 22),

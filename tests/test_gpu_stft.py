@@ -55,7 +55,7 @@ def test_stft_matches_oracle(n, hop, win):
     assert err.max() <= 2e-6
 
 
-@pytest.mark.parametrize("n", [1024, 1 << 16])
+@pytest.mark.parametrize("n", [1024, 8192, 1 << 16])   # 8192: contiguous frames take k_rows_tma
 def test_stft_hop_n_equals_records(n):
     b = 9
     sig = synth.random_samples(3, 0, b * n)
