@@ -165,6 +165,29 @@ struct RowsMinBlocks {  // CTAs per SM the register budget is sized for
     static constexpr int V = PP == 32 ? (THREADS <= 256 ? 2 : 1) : (THREADS <= 256 ? 3 : 1);
 };
 
+// W_64^j = exp(-2 pi i j / 64), j = 0..63, fp64-computed and rounded to fp32
+// (cos, -sin).  The real-record split / merge factors W_n^k, n = 2L, k = t + q T
+// as W_n^t * W_{2P}^q (n / T = 2P): the second factor, with q unrolled, is a
+// constant-bank operand (c_rw64[q * 32 / P]).
+__constant__ float2 c_rw64[64] = {
+    {1.0f, -0.0f}, {0.99518472f, -0.0980171412f}, {0.980785251f, -0.195090324f}, {0.956940353f, -0.290284663f},
+    {0.923879504f, -0.382683426f}, {0.881921291f, -0.471396744f}, {0.831469595f, -0.555570245f}, {0.773010433f, -0.634393275f},
+    {0.707106769f, -0.707106769f}, {0.634393275f, -0.773010433f}, {0.555570245f, -0.831469595f}, {0.471396744f, -0.881921291f},
+    {0.382683426f, -0.923879504f}, {0.290284663f, -0.956940353f}, {0.195090324f, -0.980785251f}, {0.0980171412f, -0.99518472f},
+    {0.0f, -1.0f}, {-0.0980171412f, -0.99518472f}, {-0.195090324f, -0.980785251f}, {-0.290284663f, -0.956940353f},
+    {-0.382683426f, -0.923879504f}, {-0.471396744f, -0.881921291f}, {-0.555570245f, -0.831469595f}, {-0.634393275f, -0.773010433f},
+    {-0.707106769f, -0.707106769f}, {-0.773010433f, -0.634393275f}, {-0.831469595f, -0.555570245f}, {-0.881921291f, -0.471396744f},
+    {-0.923879504f, -0.382683426f}, {-0.956940353f, -0.290284663f}, {-0.980785251f, -0.195090324f}, {-0.99518472f, -0.0980171412f},
+    {-1.0f, 0.0f}, {-0.99518472f, 0.0980171412f}, {-0.980785251f, 0.195090324f}, {-0.956940353f, 0.290284663f},
+    {-0.923879504f, 0.382683426f}, {-0.881921291f, 0.471396744f}, {-0.831469595f, 0.555570245f}, {-0.773010433f, 0.634393275f},
+    {-0.707106769f, 0.707106769f}, {-0.634393275f, 0.773010433f}, {-0.555570245f, 0.831469595f}, {-0.471396744f, 0.881921291f},
+    {-0.382683426f, 0.923879504f}, {-0.290284663f, 0.956940353f}, {-0.195090324f, 0.980785251f}, {-0.0980171412f, 0.99518472f},
+    {0.0f, 1.0f}, {0.0980171412f, 0.99518472f}, {0.195090324f, 0.980785251f}, {0.290284663f, 0.956940353f},
+    {0.382683426f, 0.923879504f}, {0.471396744f, 0.881921291f}, {0.555570245f, 0.831469595f}, {0.634393275f, 0.773010433f},
+    {0.707106769f, 0.707106769f}, {0.773010433f, 0.634393275f}, {0.831469595f, 0.555570245f}, {0.881921291f, 0.471396744f},
+    {0.923879504f, 0.382683426f}, {0.956940353f, 0.290284663f}, {0.980785251f, 0.195090324f}, {0.99518472f, 0.0980171412f},
+};
+
 // W_n^k of a real-record plan (n = 2L real points), fp64-computed tables:
 // W_n^k = hi[k >> lb] * lo[k & (2^lb - 1)] (csrc/real.cu's factors).
 struct RealTw {
@@ -200,11 +223,47 @@ k_rows(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
     const int b = tid / T, t = tid - (tid / T) * T;
     const TableTw<L, PP> tab{tw};
     auto addr = [&](int e) { return RowLayout::at(b * L + e); };
+    // real records: a thread's elements are k = t + q T, whose partners L - k are
+    // (T - t) + (P - 1 - q) T — element P-1-q of thread T - t — or, for t = 0,
+    // element P - q of the thread itself.  With T <= 32 a record's threads share a
+    // warp and the partner comes by shuffle.  W_n^k = W_n^t W_{2P}^q (n = 2 P T).
+    constexpr bool SHFL = REAL != 0 && T <= 32;
+    const int src_lane = ((threadIdx.x & 31) & ~(T - 1)) | ((T - t) & (T - 1));
+    float2 wt = REAL != 0 ? rt(t) : make_float2(1.f, 0.f);
+    auto wk = [&](int q) { return cmul(wt, c_rw64[q * (32 / P)]); };   // W_n^{t + q T}
+    auto partner = [&](const float2 (&a)[P], int q) {
+        float2 c;
+        c.x = __shfl_sync(0xffffffffu, a[P - 1 - q].x, src_lane);
+        c.y = __shfl_sync(0xffffffffu, a[P - 1 - q].y, src_lane);
+        return t == 0 ? a[(P - q) & (P - 1)] : c;
+    };
     for (int64_t g = blockIdx.x; g * B < nrec; g += gridDim.x) {
         const int64_t r = g * B + b;
         const bool ok = r < nrec;
         const float2* src = in + r * istride + t;
         float2 v[P];
+        // keep the P products W_n^t W_{2P}^q from being hoisted out of the loop (2P live registers)
+        if constexpr (REAL != 0) asm volatile("" : "+f"(wt.x), "+f"(wt.y));
+        if constexpr (REAL == 2 && SHFL) {
+            // C2R merge on load, partners by shuffle: Z[k] = E + i O,
+            // E = (X[k] + conj X[L-k]) / 2, O = (X[k] - conj X[L-k]) conj(W_n^k) / 2
+            float2 xin[P];
+#pragma unroll
+            for (int s = 0; s < P; ++s) xin[s] = ok ? ld_stream(src + s * T) : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int s = 0; s < P; ++s) {
+                const float2 x = xin[s], y = partner(xin, s);
+                float2 z;
+                if (s == 0 && t == 0) {
+                    z = make_float2(0.5f * (x.x + x.y), 0.5f * (x.x - x.y));      // (E[0], O[0])
+                } else {
+                    const float2 e = __fmul2_rn(cadd(x, conjf2(y)), make_float2(0.5f, 0.5f));
+                    const float2 o = cmul(__fmul2_rn(csub(x, conjf2(y)), make_float2(0.5f, 0.5f)), conjf2(wk(s)));
+                    z = cadd(e, mul_pi(o));
+                }
+                v[s] = conjf2(z);   // INV
+            }
+        } else {
 #pragma unroll
         for (int s = 0; s < P; ++s) {
             // C2R reads every element twice (as itself and as a partner): keep it cached
@@ -216,7 +275,7 @@ k_rows(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
                 } else {
                     const float2 y = ok ? __ldg(in + r * istride + (L - k)) : make_float2(0.f, 0.f);
                     const float2 e = __fmul2_rn(cadd(x, conjf2(y)), make_float2(0.5f, 0.5f));
-                    const float2 o = cmul(__fmul2_rn(csub(x, conjf2(y)), make_float2(0.5f, 0.5f)), conjf2(rt(k)));
+                    const float2 o = cmul(__fmul2_rn(csub(x, conjf2(y)), make_float2(0.5f, 0.5f)), conjf2(wk(s)));
                     x = cadd(e, mul_pi(o));                                       // Z[k] = E + i O
                 }
             }
@@ -226,8 +285,25 @@ k_rows(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
             }
             v[s] = INV ? conjf2(x) : x;
         }
+        }
         fft_engine<L, PP>(v, t, sm, addr, tab);
-        if constexpr (REAL == 1) {
+        if constexpr (REAL == 1 && SHFL) {
+            // R2C split, partners by shuffle: X[k] = E + W_n^k O (packed X[0] = (X[0], X[L]))
+            float2* dst = out + r * (int64_t)L + t;
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                const float2 a = v[q], c = partner(v, q);
+                float2 x;
+                if (q == 0 && t == 0) {
+                    x = make_float2(a.x + a.y, a.x - a.y);
+                } else {
+                    const float2 e = __fmul2_rn(cadd(a, conjf2(c)), make_float2(0.5f, 0.5f));
+                    const float2 o = mul_mi(__fmul2_rn(csub(a, conjf2(c)), make_float2(0.5f, 0.5f)));
+                    x = cadd(e, cmul(o, wk(q)));
+                }
+                if (ok) st_stream(dst + q * T, x);
+            }
+        } else if constexpr (REAL == 1) {
             __syncthreads();   // every exchange of the engine has been read
 #pragma unroll
             for (int q = 0; q < P; ++q) sm[addr(t + q * T)] = v[q];
@@ -245,7 +321,7 @@ k_rows(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
                         const float2 c = sm[addr(L - k)];
                         const float2 e = __fmul2_rn(cadd(a, conjf2(c)), make_float2(0.5f, 0.5f));
                         const float2 o = mul_mi(__fmul2_rn(csub(a, conjf2(c)), make_float2(0.5f, 0.5f)));
-                        x = cadd(e, cmul(o, rt(k)));                               // X[k] = E + W^k O
+                        x = cadd(e, cmul(o, wk(q)));                               // X[k] = E + W^k O
                     }
                     st_stream(dst + q * T, x);
                 }
