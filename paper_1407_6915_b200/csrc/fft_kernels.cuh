@@ -202,12 +202,13 @@ struct RealTw {
 // REAL = 0: complex records.  REAL = 1: real records, forward (R2C): the
 // record is the L-point complex signal x[2m] + i x[2m+1]; after its transform
 // Z the split X[k] = E + W_n^k O (E = (Z[k] + conj Z[L-k])/2, O = (Z[k] -
-// conj Z[L-k])/(2i)) is done in the same kernel, partners read from shared
-// memory, and the packed half spectrum (out[0] = (X[0], X[L])) is stored.
-// REAL = 2: inverse (C2R): the merge Z[k] = E + i O (E = (X[k] + conj
-// X[L-k])/2, O = (X[k] - conj X[L-k]) conj(W_n^k)/2) happens on load (the
-// partner read straight from global memory), then the inverse transform.
-// csrc/real.cu holds the same arithmetic as separate kernels for longer records.
+// conj Z[L-k])/(2i)) is done in the same kernel and the packed half spectrum
+// (out[0] = (X[0], X[L])) is stored.  REAL = 2: inverse (C2R): the merge
+// Z[k] = E + i O (E = (X[k] + conj X[L-k])/2, O = (X[k] - conj X[L-k])
+// conj(W_n^k)/2) happens on load, then the inverse transform.  Partners come
+// by warp shuffle when a record's T threads share a warp (T <= 32), else
+// through shared memory.  csrc/real.cu holds the same arithmetic as separate
+// kernels for longer records.
 template <int L, int B, bool INV, int PP = 16, int MINB = 0, int REAL = 0>   // MINB > 0 overrides the register budget
 __global__ void __launch_bounds__(B * Sched<L, PP>::T, MINB > 0 ? MINB : RowsMinBlocks<L, B, PP>::V)
 k_rows(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
@@ -263,22 +264,35 @@ k_rows(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec,
                 }
                 v[s] = conjf2(z);   // INV
             }
+        } else if constexpr (REAL == 2) {
+            // C2R merge on load, partners through shared memory (the record's
+            // threads span several warps)
+            float2 xin[P];
+#pragma unroll
+            for (int s = 0; s < P; ++s) xin[s] = ok ? ld_stream(src + s * T) : make_float2(0.f, 0.f);
+            __syncthreads();   // the previous record's last exchange has been read
+#pragma unroll
+            for (int s = 0; s < P; ++s) sm[addr(t + s * T)] = xin[s];
+            __syncthreads();
+#pragma unroll
+            for (int s = 0; s < P; ++s) {
+                const int k = t + s * T;
+                const float2 x = xin[s];
+                float2 z;
+                if (k == 0) {
+                    z = make_float2(0.5f * (x.x + x.y), 0.5f * (x.x - x.y));      // (E[0], O[0])
+                } else {
+                    const float2 y = sm[addr(L - k)];
+                    const float2 e = __fmul2_rn(cadd(x, conjf2(y)), make_float2(0.5f, 0.5f));
+                    const float2 o = cmul(__fmul2_rn(csub(x, conjf2(y)), make_float2(0.5f, 0.5f)), conjf2(wk(s)));
+                    z = cadd(e, mul_pi(o));
+                }
+                v[s] = conjf2(z);   // INV
+            }
         } else {
 #pragma unroll
         for (int s = 0; s < P; ++s) {
-            // C2R reads every element twice (as itself and as a partner): keep it cached
-            float2 x = ok ? (REAL == 2 ? __ldg(src + s * T) : ld_stream(src + s * T)) : make_float2(0.f, 0.f);
-            if constexpr (REAL == 2) {
-                const int k = t + s * T;
-                if (k == 0) {
-                    x = make_float2(0.5f * (x.x + x.y), 0.5f * (x.x - x.y));      // (E[0], O[0])
-                } else {
-                    const float2 y = ok ? __ldg(in + r * istride + (L - k)) : make_float2(0.f, 0.f);
-                    const float2 e = __fmul2_rn(cadd(x, conjf2(y)), make_float2(0.5f, 0.5f));
-                    const float2 o = cmul(__fmul2_rn(csub(x, conjf2(y)), make_float2(0.5f, 0.5f)), conjf2(wk(s)));
-                    x = cadd(e, mul_pi(o));                                       // Z[k] = E + i O
-                }
-            }
+            float2 x = ok ? ld_stream(src + s * T) : make_float2(0.f, 0.f);
             if (window) {
                 const float w = __ldg(window + t + s * T);
                 x = make_float2(x.x * w, x.y * w);
