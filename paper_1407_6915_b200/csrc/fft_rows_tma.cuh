@@ -1,6 +1,6 @@
 // fft_rows_tma.cuh — engine E1 (single pass) for the
 // longest records that still fit one CTA, with the record loads taken off the
-// compute warps: a producer warp streams whole records into an NSTAGE-deep
+// compute warps' critical path: whole records are streamed into an NSTAGE-deep
 // ring of shared-memory stages with bulk copies (TMA), and NGRP compute groups
 // of T = L / PP threads each FFT one staged record in place (the engine's
 // exchanges reuse the stage) and store the result straight from registers.
@@ -12,8 +12,11 @@
 //
 // Records are dealt statically: CTA c takes records c, c + grid, ...; task k
 // of a CTA is its k-th record, staged in stage k mod NSTAGE and computed by
-// group k mod NGRP.  full[s] completes when the copy lands; empty[s] when every
-// warp of the computing group has read the stage for the last time.
+// group k mod NGRP.  There is no producer warp (17 warps would cap registers
+// at 96 per thread: 5 warps on one SM sub-partition): thread 0 stages the first
+// NSTAGE records, and the group that has read stage s for the last time
+// (group barrier) refills it with task k + NSTAGE; full[s] completes when a
+// copy lands.
 #pragma once
 
 #include "fft_pipe.cuh"
@@ -33,73 +36,118 @@ template <int L, int PP, int NGRP, int NSTAGE>
 struct RowsTmaCfg {
     using S = Sched<L, PP>;
     static constexpr int T = S::T;                                     // threads per record (one group)
-    static constexpr int NT = NGRP * T + 32;                           // + producer warp
+    static constexpr int NT = NGRP * T;
     static constexpr int STAGE = (RowLayout::size(L) + 15) / 16 * 16;  // entries per stage (padded exchanges)
     static constexpr int CHUNKS = L * 8 >= 4 * 16384 ? 4 : 1;          // bulk copies per record
-    static constexpr size_t SMEM = sizeof(float2) * (size_t)STAGE * NSTAGE + 16 * NSTAGE;
+    static constexpr size_t SMEM = sizeof(float2) * (size_t)STAGE * NSTAGE + 8 * NSTAGE;
     static constexpr int MINB = SMEM * 2 <= 227 * 1024 ? 2 : 1;
-    static_assert(T % 32 == 0 && NGRP <= NSTAGE && (L / CHUNKS) % 2 == 0, "stage geometry");
+    static_assert(T % 32 == 0 && NGRP <= NSTAGE && (L / CHUNKS) % 2 == 0 && CHUNKS <= T, "stage geometry");
 };
 
-template <int L, bool INV, int PP, int NGRP, int NSTAGE>
+// REAL (as k_rows): 0 complex records; 1 real records forward (R2C split after
+// the transform, partners exchanged through the stage); 2 real records inverse
+// (C2R merge before it: the record is staged in natural order, so the partner
+// X[L-k] is read straight from the stage).
+template <int L, bool INV, int PP, int NGRP, int NSTAGE, int REAL = 0>
 __global__ void __launch_bounds__(RowsTmaCfg<L, PP, NGRP, NSTAGE>::NT, RowsTmaCfg<L, PP, NGRP, NSTAGE>::MINB)
 k_rows_tma(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec, const float2* __restrict__ tw,
-           float scale) {
+           float scale, RealTw rt) {
+    static_assert(REAL == 0 || INV == (REAL == 2), "R2C is forward, C2R inverse");
     using CF = RowsTmaCfg<L, PP, NGRP, NSTAGE>;
     constexpr int T = CF::T, P = CF::S::P, STAGE = CF::STAGE;
     extern __shared__ __align__(128) float2 sm[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + (size_t)STAGE * NSTAGE);   // full | empty
-    const uint32_t full0 = smem_addr(bars), empty0 = smem_addr(bars + NSTAGE);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + (size_t)STAGE * NSTAGE);   // full[NSTAGE]
+    const uint32_t full0 = smem_addr(bars);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t G = gridDim.x;
+    const uint64_t pol = policy_evict_first();
+    // stage task k (record blockIdx.x + k G) into stage k mod NSTAGE: CHUNKS bulk
+    // copies issued by lanes 0..CHUNKS-1 of the calling warp
+    auto stage_task = [&](uint32_t k) {
+        const int64_t r = blockIdx.x + (int64_t)k * G;
+        if (r >= nrec) return;
+        const uint32_t s = k % NSTAGE;
+        if (lane == 0) mbar_expect_tx(full0 + 8 * s, (uint32_t)(L * sizeof(float2)));
+        __syncwarp();
+        constexpr int CH = L / CF::CHUNKS;
+        if (lane < CF::CHUNKS)
+            bulk_g2s_hint(smem_addr(sm + (size_t)s * STAGE + lane * CH), in + r * L + lane * CH, CH * sizeof(float2),
+                          full0 + 8 * s, pol);
+    };
     if (tid == 0) {
-        for (int i = 0; i < NSTAGE; ++i) {
-            mbar_init(full0 + 8 * i, 1);
-            mbar_init(empty0 + 8 * i, T / 32);   // one arrival per warp of the computing group
-        }
+        for (int i = 0; i < NSTAGE; ++i) mbar_init(full0 + 8 * i, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const int64_t G = gridDim.x;
-    if (warp == NGRP * T / 32) {
-        // ============================================== producer
-        const uint64_t pol = policy_evict_first();
-        uint32_t k = 0;
-        for (int64_t r = blockIdx.x; r < nrec; r += G, ++k) {
-            const uint32_t s = k % NSTAGE, u = k / NSTAGE;
-            if (lane == 0) {
-                if (u > 0) mbar_wait(empty0 + 8 * s, (u - 1) & 1);
-                mbar_expect_tx(full0 + 8 * s, (uint32_t)(L * sizeof(float2)));
-            }
-            __syncwarp();
-            constexpr int CH = L / CF::CHUNKS;
-            if (lane < CF::CHUNKS)
-                bulk_g2s_hint(smem_addr(sm + (size_t)s * STAGE + lane * CH), in + r * L + lane * CH,
-                              CH * sizeof(float2), full0 + 8 * s, pol);
-        }
-    } else {
+    if (warp == 0)
+        for (uint32_t k = 0; k < NSTAGE; ++k) stage_task(k);
+    {
         // ============================================== compute groups
         const int grp = warp / (T / 32);
         const int t = tid - grp * T;
         const NamedBarrier bar{1 + grp, T};
         const TableTw<L, PP> tab{tw};
+        // real records: W_n^k = W_n^t W_{2P}^q for k = t + q T (n = 2 P T; fft_kernels.cuh)
+        float2 wt = REAL != 0 ? rt(t) : make_float2(1.f, 0.f);
+        auto wk = [&](int q) { return cmul(wt, c_rw64[q * (32 / P)]); };
         uint32_t k = grp;
         for (int64_t r = blockIdx.x + (int64_t)grp * G; r < nrec; r += NGRP * G, k += NGRP) {
             const uint32_t s = k % NSTAGE, u = k / NSTAGE;
             float2* stage = sm + (size_t)s * STAGE;
+            if constexpr (REAL != 0) asm volatile("" : "+f"(wt.x), "+f"(wt.y));   // not hoisted: 2P registers
             mbar_wait(full0 + 8 * s, u & 1);
             float2 v[P];
 #pragma unroll
             for (int j = 0; j < P; ++j) {
                 const float2 x = stage[t + j * T];
-                v[j] = INV ? conjf2(x) : x;
+                if constexpr (REAL == 2) {
+                    // Z[k] = E + i O, E = (X[k] + conj X[L-k]) / 2, O = (X[k] - conj X[L-k]) conj(W_n^k) / 2
+                    const int kk = t + j * T;
+                    float2 z;
+                    if (kk == 0) {
+                        z = make_float2(0.5f * (x.x + x.y), 0.5f * (x.x - x.y));
+                    } else {
+                        const float2 y = stage[L - kk];
+                        const float2 e = __fmul2_rn(cadd(x, conjf2(y)), make_float2(0.5f, 0.5f));
+                        const float2 o = cmul(__fmul2_rn(csub(x, conjf2(y)), make_float2(0.5f, 0.5f)), conjf2(wk(j)));
+                        z = cadd(e, mul_pi(o));
+                    }
+                    v[j] = conjf2(z);
+                } else {
+                    v[j] = INV ? conjf2(x) : x;
+                }
             }
             fft_engine<L, PP>(v, t, stage, [](int e) { return RowLayout::at(e); }, tab, bar);
-            fence_proxy_async_smem();   // last generic access of the stage: before its next bulk refill
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty0 + 8 * s);
             float2* dst = out + r * L + t;
+            if constexpr (REAL == 1) {
+                // X[k] = E + W_n^k O, E = (Z[k] + conj Z[L-k]) / 2, O = (Z[k] - conj Z[L-k]) / (2i); out[0] = (X[0], X[L])
+                bar();   // the engine's last exchange has been read by the whole group
 #pragma unroll
-            for (int q = 0; q < P; ++q) st_stream(dst + q * T, INV ? scale_conj(v[q], scale) : v[q]);
+                for (int q = 0; q < P; ++q) stage[RowLayout::at(t + q * T)] = v[q];
+                bar();
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    const float2 a = v[q], c = stage[RowLayout::at((L - (t + q * T)) & (L - 1))];
+                    float2 x;
+                    if (q == 0 && t == 0) {
+                        x = make_float2(a.x + a.y, a.x - a.y);
+                    } else {
+                        const float2 e = __fmul2_rn(cadd(a, conjf2(c)), make_float2(0.5f, 0.5f));
+                        const float2 o = mul_mi(__fmul2_rn(csub(a, conjf2(c)), make_float2(0.5f, 0.5f)));
+                        x = cadd(e, cmul(o, wk(q)));
+                    }
+                    st_stream(dst + q * T, x);
+                }
+                fence_proxy_async_smem();   // this thread's last generic access of the stage
+                bar();
+                if (t < 32) stage_task(k + NSTAGE);   // the group's first warp refills it
+            } else {
+                fence_proxy_async_smem();   // this thread's last generic access of the stage
+                bar();
+                if (t < 32) stage_task(k + NSTAGE);   // the group's first warp refills it
+#pragma unroll
+                for (int q = 0; q < P; ++q) st_stream(dst + q * T, INV ? scale_conj(v[q], scale) : v[q]);
+            }
         }
     }
 }

@@ -75,13 +75,17 @@ KernelSet pick_row(int log2l, bool inv) {
         default: return KernelSet{};
     }
 }
-// k_rows_tma (fft_rows_tma.cuh): records streamed into shared-memory stages by a
-// producer warp; two compute groups over three 68 KiB stages at 2^13 (79.8 %
-// vs k_rows 73.9 %; 2^12 and shorter gain nothing: profiles/r02_rows_tma.txt)
-template <int L, int PP, int NGRP, int NSTAGE> static KernelSet row_tma_kernel(bool inv) {
+// k_rows_tma (fft_rows_tma.cuh): records streamed into shared-memory stages by
+// bulk copies; two compute groups over three 68 KiB stages at 2^13 (85.7 % vs
+// k_rows 73.9 %; 2^12 and shorter gain nothing: profiles/r02_rows_tma.txt)
+template <int L, int PP, int NGRP, int NSTAGE, bool REAL = false> static KernelSet row_tma_kernel(bool inv) {
     using CF = RowsTmaCfg<L, PP, NGRP, NSTAGE>;
     KernelSet k;
-    k.fn = inv ? (const void*)&k_rows_tma<L, true, PP, NGRP, NSTAGE> : (const void*)&k_rows_tma<L, false, PP, NGRP, NSTAGE>;
+    if constexpr (REAL)
+        k.fn = inv ? (const void*)&k_rows_tma<L, true, PP, NGRP, NSTAGE, 2>
+                   : (const void*)&k_rows_tma<L, false, PP, NGRP, NSTAGE, 1>;
+    else
+        k.fn = inv ? (const void*)&k_rows_tma<L, true, PP, NGRP, NSTAGE> : (const void*)&k_rows_tma<L, false, PP, NGRP, NSTAGE>;
     k.threads = CF::NT;
     k.smem = CF::SMEM;
     k.cols = 1;
@@ -91,6 +95,14 @@ template <int L, int PP, int NGRP, int NSTAGE> static KernelSet row_tma_kernel(b
 KernelSet pick_row_tma(int log2l, bool inv) {
     switch (log2l) {
         case 13: return row_tma_kernel<8192, 32, 2, 3>(inv);
+        default: return KernelSet{};
+    }
+}
+// the staged kernel with the real-record split / merge fused (real records of
+// 2^(log2l+1) samples), or an empty set
+KernelSet pick_row_real_tma(int log2l, bool inv) {
+    switch (log2l) {
+        case 13: return row_tma_kernel<8192, 32, 2, 3, true>(inv);
         default: return KernelSet{};
     }
 }

@@ -516,6 +516,18 @@ extern "C" fft_plan* fft_plan_create_real(int64_t n, int64_t batch, int dir) {
             return fail();
         }
         p->occ_a = std::max(p->occ_a, 1);
+        // 2^14 reals: the staged kernel (k_rows_tma<..., REAL>) when the inner plan uses it
+        if (p->inner->kt.fn) {
+            p->kt = pick_row_real_tma(ilog2((int)(n / 2)), dir == FFT_INVERSE);
+            if (p->kt.fn) {
+                if (set_smem(p->kt)) return fail();
+                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ_t, p->kt.fn, p->kt.threads, p->kt.smem);
+                if (e != cudaSuccess || p->occ_t < 1) {
+                    bfft_set_error(FFT_E_CUDA, "k_rows_tma (real) cannot be scheduled");
+                    return fail();
+                }
+            }
+        }
     }
     return p;
 }
@@ -623,7 +635,8 @@ static int launch(const fft_plan* p, const float2* in, float2* out, int64_t coun
                 // contiguous records: persistent staged kernel, one CTA per SM slot
                 const int grid = (int)std::min<int64_t>(count, (int64_t)p->sms * p->occ_t);
                 if (grid > 0)
-                    ((RowTmaFn)p->kt.fn)<<<grid, p->kt.threads, p->kt.smem, st>>>(in, out, count, p->tw_a, p->scale);
+                    ((RowTmaFn)p->kt.fn)<<<grid, p->kt.threads, p->kt.smem, st>>>(in, out, count, p->tw_a, p->scale,
+                                                                                   RealTw{nullptr, nullptr, 0});
                 break;
             }
             const int64_t groups = (count + p->ka.cols - 1) / p->ka.cols;
@@ -736,6 +749,15 @@ extern "C" int fft_exec_range(const fft_plan* p, const void* in, void* out, int6
         // inverse = the merge into `out`, then the complex inverse in place
         const int64_t h = p->n / 2;
         cudaStream_t st = (cudaStream_t)stream;
+        if (p->kt.fn) {   // fused staged kernel
+            const int grid = (int)std::min<int64_t>(count, (int64_t)p->sms * p->occ_t);
+            if (grid > 0)
+                ((RowTmaFn)p->kt.fn)<<<grid, p->kt.threads, p->kt.smem, st>>>(
+                    (const float2*)in, (float2*)out, count, p->inner->tw_a, p->inner->scale, RealTw{p->tw_a, p->tw_b, p->rt_lb});
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return bfft_set_error(FFT_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+            return FFT_OK;
+        }
         if (p->ka.fn) {   // fused single-pass kernel
             const int64_t groups = (count + p->ka.cols - 1) / p->ka.cols;
             const int grid = (int)std::min<int64_t>(groups, (int64_t)p->sms * p->occ_a * 8);

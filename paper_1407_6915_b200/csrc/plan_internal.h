@@ -31,7 +31,7 @@ struct ClusterChoice {
 
 // kernel signatures, by family (launch casts KernelSet::fn to these)
 using RowFn = void (*)(const float2*, float2*, int64_t, const float2*, float, int64_t, const float*, bfft::RealTw);
-using RowTmaFn = void (*)(const float2*, float2*, int64_t, const float2*, float);
+using RowTmaFn = void (*)(const float2*, float2*, int64_t, const float2*, float, bfft::RealTw);
 using ColFn = void (*)(const float2*, float2*, int64_t, int, const float2*);
 using RowTFn = void (*)(const float2*, float2*, int64_t, int, const float2*, float);
 using ClusterFn = void (*)(const CUtensorMap, float2*, int64_t, const float2*, const float2*, float);
@@ -48,6 +48,7 @@ KernelSet pick_row(int log2l, bool inv);
 // kern_rows.cu: the staged single-pass kernel (k_rows_tma) for 2^log2l, or an
 // empty set where k_rows is the faster kernel (same twiddle table as pick_row)
 KernelSet pick_row_tma(int log2l, bool inv);
+KernelSet pick_row_real_tma(int log2l, bool inv);
 // kern_rows.cu: the single-pass kernel with the real-record split (R2C, !inv)
 // or merge (C2R, inv) fused, for real records of n = 2^(log2l+1) points
 KernelSet pick_row_real(int log2l, bool inv);
