@@ -64,7 +64,9 @@ def test_r2c_forward_matches_oracle(n):
     assert err.max() <= 2e-6, err.max()        # quality band (as for complex records)
 
 
-@pytest.mark.parametrize("n", [4, 8, 1024, 4096, 1 << 14, 1 << 16, 1 << 20, 1 << 23])
+# 64..1024: partners by warp shuffle at T = 2..32 threads per record; 2048..8192:
+# through shared memory; 2^14: the staged kernel (k_rows_tma); longer: two kernels
+@pytest.mark.parametrize("n", [4, 8, 64, 256, 512, 1024, 2048, 4096, 8192, 1 << 14, 1 << 16, 1 << 20, 1 << 23])
 def test_c2r_inverse_matches_oracle(n):
     b = 2 if n >= (1 << 21) else 5
     x = real_records(2000 + n, n, b)
@@ -79,6 +81,30 @@ def test_c2r_inverse_matches_oracle(n):
     # round trip to the original reals
     assert np.all(oracle.rel_l2(z.cpu().numpy().astype(np.complex128), x.astype(np.complex128))
                   <= oracle.tolerance(n))
+
+
+@pytest.mark.parametrize("direction", [-1, 1])
+def test_real_staged_kernel_reuses_stages(direction):
+    # 2^14 reals on k_rows_tma: 449 records = three or more per persistent CTA, so
+    # every stage is refilled and both groups alternate (R2C split through the
+    # stage; C2R merge from the natural-order stage)
+    n, b = 1 << 14, 449
+    x = real_records(3000 + n, n, b)
+    full = oracle.records_c64(x.astype(np.complex64), oracle.FORWARD)
+    if direction == bf.FFT_FORWARD:
+        with bf.RealPlan(n, b) as p:
+            y = p.exec(torch.from_numpy(x).cuda())
+        torch.cuda.synchronize()
+        err = oracle.rel_l2(y.cpu().numpy(), packed_from_full(full))
+    else:
+        P = packed_from_full(full).astype(np.complex64)
+        with bf.RealPlan(n, b, bf.FFT_INVERSE) as p:
+            z = p.exec(torch.from_numpy(P).cuda())
+        torch.cuda.synchronize()
+        ref = oracle.records_c64(full_from_packed(P.astype(np.complex128)).astype(np.complex64), oracle.INVERSE)
+        err = oracle.rel_l2(z.cpu().numpy().astype(np.complex128), ref.real.astype(np.complex128))
+    assert np.all(err <= oracle.tolerance(n)), err.max()
+    assert err.max() <= 2e-6, err.max()
 
 
 def test_r2c_closed_forms_and_in_place():
