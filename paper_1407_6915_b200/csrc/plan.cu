@@ -605,7 +605,7 @@ extern "C" int fft_plan_get_info(const fft_plan* p, fft_plan_info* info) {
     info->cluster = p->cluster;
     info->scratch_bytes = p->d_scratch ? p->wave * p->n * 8 : 0;
     info->table_bytes = (int64_t)p->tab_bytes;
-    info->resident = p->occ_a;
+    info->resident = p->kt.fn ? p->occ_t : p->occ_a;   // the kernel a contiguous exec launches
     info->exclusive = (p->variant == FFT_VARIANT_PIPE || p->variant == FFT_VARIANT_FOURSTEP) ? 1 : 0;
     info->ring_records = p->variant == FFT_VARIANT_PIPE ? p->pipe_S : 0;
     info->ring_lag = p->variant == FFT_VARIANT_PIPE ? p->pipe_LAG : 0;
