@@ -101,8 +101,8 @@ fft_plan *fft_plan_create_ex(int64_t n, int64_t batch, int dir, int variant);
 typedef struct fft_plan_opts {
     int variant;      /* enum fft_variant (0 = auto)                          */
     int impl;         /* implementation inside the variant, 0 = default:
-                         FFT_VARIANT_SINGLE  1 k_rows, 2 k_rows_tma (2^13;
-                                             records staged by TMA);
+                         FFT_VARIANT_SINGLE  1 k_rows, 2 the staged kernels
+                                             (k_rows_tma 2^13, k_rows_tma2 2^14);
                          FFT_VARIANT_PIPE    1 k_pipe, 2 k_pipe2, 3 k_pipe3;
                          FFT_VARIANT_CLUSTER 1 k_cluster1 (single buffer),
                                              2 k_cluster2 (pipelined),
@@ -159,7 +159,7 @@ fft_plan *fft_plan_create_real(int64_t n, int64_t batch, int dir);
  * skips samples), else FFT_E_ARG; n, frames, dir as in fft_plan_create.
  * fft_exec(plan, in, out, stream): in = the signal, (frames-1)*hop + n
  * complex64 samples; out = frames*n complex64; in and out must not overlap.
- * Frames of up to 2^13 points are framed and windowed on load by the
+ * Frames of up to 2^14 points are framed and windowed on load by the
  * single-pass kernel (one launch); longer frames are framed into out by one
  * more kernel and transformed in place.
  */

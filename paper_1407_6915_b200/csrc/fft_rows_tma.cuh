@@ -153,3 +153,128 @@ k_rows_tma(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec
 }
 
 }  // namespace bfft
+
+namespace bfft {
+
+// k_rows_tma2: the same idea for records too long for two stages (2^14: 128 KiB
+// plus exchange padding).  The record's exchange buffer X holds its last
+// L - YL points in place; the first YL points are staged in a separate buffer
+// Y.  Y is refilled with the next record's head as soon as the transform's
+// inputs are in registers; X's tail is refilled once the engine's last
+// exchange has been read — only that tail's arrival is exposed.  One group of
+// T = L / PP threads per CTA.
+template <int L, int PP, int YL>
+struct RowsTma2Cfg {
+    using S = Sched<L, PP>;
+    static constexpr int T = S::T, NT = T;
+    static constexpr int XS = (RowLayout::size(L) + 15) / 16 * 16;
+    static constexpr size_t SMEM = sizeof(float2) * (size_t)(XS + YL) + 16;
+    static_assert(YL % T == 0 && YL % 8 == 0 && (L - YL) % 8 == 0, "head / tail split");
+};
+
+// REAL as k_rows_tma (1 R2C split through X after the transform, 2 C2R merge
+// on load with the partner read from Y or X).
+template <int L, bool INV, int PP, int YL, int REAL = 0>
+__global__ void __launch_bounds__(RowsTma2Cfg<L, PP, YL>::NT, 1)
+k_rows_tma2(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec, const float2* __restrict__ tw,
+            float scale, RealTw rt) {
+    static_assert(REAL == 0 || INV == (REAL == 2), "R2C is forward, C2R inverse");
+    using CF = RowsTma2Cfg<L, PP, YL>;
+    constexpr int T = CF::T, P = CF::S::P, XS = CF::XS, JY = YL / T;
+    extern __shared__ __align__(128) float2 sm[];
+    float2* X = sm;
+    float2* Y = sm + XS;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Y + YL);   // fullY, fullX
+    const uint32_t fullY = smem_addr(bars), fullX = smem_addr(bars + 1);
+    const int t = threadIdx.x, lane = t & 31;
+    const int64_t G = gridDim.x;
+    const uint64_t pol = policy_evict_first();
+    // bulk copy of [lo, hi) of record r into dst, lanes 0..3 of warp 0
+    auto load = [&](float2* dst, int64_t r, int lo, int hi, uint32_t bar) {
+        if (lane == 0) mbar_expect_tx(bar, (uint32_t)((hi - lo) * sizeof(float2)));
+        __syncwarp();
+        const int ch = (hi - lo) / 4;
+        if (lane < 4)
+            bulk_g2s_hint(smem_addr(dst + lane * ch), in + r * L + lo + lane * ch, ch * sizeof(float2), bar, pol);
+    };
+    if (t == 0) {
+        mbar_init(fullY, 1);
+        mbar_init(fullX, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t < 32 && (int64_t)blockIdx.x < nrec) {
+        load(Y, blockIdx.x, 0, YL, fullY);
+        load(X + YL, blockIdx.x, YL, L, fullX);
+    }
+    const CtaBarrier bar{};
+    const TableTw<L, PP> tab{tw};
+    // real records: W_n^k = W_n^t W_{2P}^q for k = t + q T (n = 2 P T; fft_kernels.cuh)
+    float2 wt = REAL != 0 ? rt(t) : make_float2(1.f, 0.f);
+    auto wk = [&](int q) { return cmul(wt, c_rw64[q * (32 / P)]); };
+    uint32_t k = 0;
+    for (int64_t r = blockIdx.x; r < nrec; r += G, ++k) {
+        const bool more = r + G < nrec;
+        if constexpr (REAL != 0) asm volatile("" : "+f"(wt.x), "+f"(wt.y));   // not hoisted: 2P registers
+        mbar_wait(fullY, k & 1);
+        mbar_wait(fullX, k & 1);
+        float2 v[P];
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            const float2 x = j < JY ? Y[t + j * T] : X[t + j * T];
+            if constexpr (REAL == 2) {
+                // Z[k] = E + i O, E = (X[k] + conj X[L-k]) / 2, O = (X[k] - conj X[L-k]) conj(W_n^k) / 2
+                const int kk = t + j * T;
+                float2 z;
+                if (kk == 0) {
+                    z = make_float2(0.5f * (x.x + x.y), 0.5f * (x.x - x.y));
+                } else {
+                    const int pk = L - kk;
+                    const float2 y = pk < YL ? Y[pk] : X[pk];
+                    const float2 e = __fmul2_rn(cadd(x, conjf2(y)), make_float2(0.5f, 0.5f));
+                    const float2 o = cmul(__fmul2_rn(csub(x, conjf2(y)), make_float2(0.5f, 0.5f)), conjf2(wk(j)));
+                    z = cadd(e, mul_pi(o));
+                }
+                v[j] = conjf2(z);
+            } else {
+                v[j] = INV ? conjf2(x) : x;
+            }
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (t < 32 && more) load(Y, r + G, 0, YL, fullY);   // the next head, behind this transform
+        fft_engine<L, PP>(v, t, X, [](int e) { return RowLayout::at(e); }, tab, bar);
+        float2* dst = out + r * L + t;
+        if constexpr (REAL == 1) {
+            // X[k] = E + W_n^k O, E = (Z[k] + conj Z[L-k]) / 2, O = (Z[k] - conj Z[L-k]) / (2i); out[0] = (X[0], X[L])
+            __syncthreads();   // the engine's last exchange has been read
+#pragma unroll
+            for (int q = 0; q < P; ++q) X[RowLayout::at(t + q * T)] = v[q];
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                const float2 a = v[q], c = X[RowLayout::at((L - (t + q * T)) & (L - 1))];
+                float2 x;
+                if (q == 0 && t == 0) {
+                    x = make_float2(a.x + a.y, a.x - a.y);
+                } else {
+                    const float2 e = __fmul2_rn(cadd(a, conjf2(c)), make_float2(0.5f, 0.5f));
+                    const float2 o = mul_mi(__fmul2_rn(csub(a, conjf2(c)), make_float2(0.5f, 0.5f)));
+                    x = cadd(e, cmul(o, wk(q)));
+                }
+                st_stream(dst + q * T, x);
+            }
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (t < 32 && more) load(X + YL, r + G, YL, L, fullX);
+        } else {
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (t < 32 && more) load(X + YL, r + G, YL, L, fullX);   // the next tail, behind the stores
+#pragma unroll
+            for (int q = 0; q < P; ++q) st_stream(dst + q * T, INV ? scale_conj(v[q], scale) : v[q]);
+        }
+    }
+}
+
+}  // namespace bfft

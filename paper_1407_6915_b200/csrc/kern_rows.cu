@@ -92,9 +92,26 @@ template <int L, int PP, int NGRP, int NSTAGE, bool REAL = false> static KernelS
     k.pp = PP;
     return k;
 }
+// 2^14: one record per CTA, its head staged apart from the exchange buffer
+// (k_rows_tma2, 73 % vs k_pipe2 63 %: profiles/r02_rows_tma.txt)
+constexpr int TMA2_HEAD = 10240;
+template <int L, int PP, int YL, bool REAL = false> static KernelSet row_tma2_kernel(bool inv) {
+    using CF = RowsTma2Cfg<L, PP, YL>;
+    KernelSet k;
+    if constexpr (REAL)
+        k.fn = inv ? (const void*)&k_rows_tma2<L, true, PP, YL, 2> : (const void*)&k_rows_tma2<L, false, PP, YL, 1>;
+    else
+        k.fn = inv ? (const void*)&k_rows_tma2<L, true, PP, YL> : (const void*)&k_rows_tma2<L, false, PP, YL>;
+    k.threads = CF::NT;
+    k.smem = CF::SMEM;
+    k.cols = 1;
+    k.pp = PP;
+    return k;
+}
 KernelSet pick_row_tma(int log2l, bool inv) {
     switch (log2l) {
         case 13: return row_tma_kernel<8192, 32, 2, 3>(inv);
+        case 14: return row_tma2_kernel<16384, 32, TMA2_HEAD>(inv);
         default: return KernelSet{};
     }
 }
@@ -103,6 +120,7 @@ KernelSet pick_row_tma(int log2l, bool inv) {
 KernelSet pick_row_real_tma(int log2l, bool inv) {
     switch (log2l) {
         case 13: return row_tma_kernel<8192, 32, 2, 3, true>(inv);
+        case 14: return row_tma2_kernel<16384, 32, TMA2_HEAD, true>(inv);
         default: return KernelSet{};
     }
 }

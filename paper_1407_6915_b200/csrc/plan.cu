@@ -185,7 +185,9 @@ static int validate(int64_t n, int64_t batch, int dir, bool dir_ok_zero = false)
 }
 
 // fastest measured per size (profiles/r01_variants_*.txt)
-static int default_variant(int log2n) { return log2n <= 13 ? FFT_VARIANT_SINGLE : FFT_VARIANT_PIPE; }
+// single pass up to 2^14 (k_rows, k_rows_tma at 2^13, k_rows_tma2 at 2^14), the
+// pipelined four-step above (profiles/r02_config5_sweep_final.txt)
+static int default_variant(int log2n) { return log2n <= 14 ? FFT_VARIANT_SINGLE : FFT_VARIANT_PIPE; }
 
 static int set_smem(const KernelSet& k) {
     if (k.smem > 48 * 1024)
@@ -504,29 +506,29 @@ extern "C" fft_plan* fft_plan_create_real(int64_t n, int64_t batch, int dir) {
     if (p->inner->variant == FFT_VARIANT_SINGLE) {
         // records of up to 2^14 reals: one kernel, the split / merge fused into the
         // single-pass transform (k_rows<..., REAL>); longer records: two kernels
-        p->ka = pick_row_real(ilog2((int)(n / 2)), dir == FFT_INVERSE);
-        if (!p->ka.fn) {
-            bfft_set_error(FFT_E_SIZE, "unsupported transform size: %lld", (long long)n);
-            return fail();
-        }
-        if (set_smem(p->ka)) return fail();
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ_a, p->ka.fn, p->ka.threads, p->ka.smem);
-        if (e != cudaSuccess) {
-            bfft_set_error(FFT_E_CUDA, "occupancy query failed: %s", cudaGetErrorString(e));
-            return fail();
-        }
-        p->occ_a = std::max(p->occ_a, 1);
-        // 2^14 reals: the staged kernel (k_rows_tma<..., REAL>) when the inner plan uses it
-        if (p->inner->kt.fn) {
-            p->kt = pick_row_real_tma(ilog2((int)(n / 2)), dir == FFT_INVERSE);
-            if (p->kt.fn) {
-                if (set_smem(p->kt)) return fail();
-                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ_t, p->kt.fn, p->kt.threads, p->kt.smem);
-                if (e != cudaSuccess || p->occ_t < 1) {
-                    bfft_set_error(FFT_E_CUDA, "k_rows_tma (real) cannot be scheduled");
-                    return fail();
-                }
+        // 2^14 / 2^15 reals: the staged kernels (k_rows_tma / k_rows_tma2 <..., REAL>) when the
+        // inner plan uses them; else k_rows<..., REAL>
+        if (p->inner->kt.fn) p->kt = pick_row_real_tma(ilog2((int)(n / 2)), dir == FFT_INVERSE);
+        if (p->kt.fn) {
+            if (set_smem(p->kt)) return fail();
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ_t, p->kt.fn, p->kt.threads, p->kt.smem);
+            if (e != cudaSuccess || p->occ_t < 1) {
+                bfft_set_error(FFT_E_CUDA, "k_rows_tma (real) cannot be scheduled");
+                return fail();
             }
+        } else {
+            p->ka = pick_row_real(ilog2((int)(n / 2)), dir == FFT_INVERSE);
+            if (!p->ka.fn) {
+                bfft_set_error(FFT_E_SIZE, "unsupported transform size: %lld", (long long)n);
+                return fail();
+            }
+            if (set_smem(p->ka)) return fail();
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ_a, p->ka.fn, p->ka.threads, p->ka.smem);
+            if (e != cudaSuccess) {
+                bfft_set_error(FFT_E_CUDA, "occupancy query failed: %s", cudaGetErrorString(e));
+                return fail();
+            }
+            p->occ_a = std::max(p->occ_a, 1);
         }
     }
     return p;
@@ -581,7 +583,7 @@ extern "C" int fft_plan_get_info(const fft_plan* p, fft_plan_info* info) {
         int rc = fft_plan_get_info(p->inner, info);
         info->n = p->n;
         info->dir = p->dir;
-        if (!p->ka.fn) info->kernels_per_exec += 1;  // + the split / merge kernel (fused up to 2^14)
+        if (!p->ka.fn && !p->kt.fn) info->kernels_per_exec += 1;  // + the split / merge kernel (fused up to 2^15)
         info->table_bytes += (int64_t)p->tab_bytes;
         info->real = 1;
         info->hop = 0;

@@ -145,7 +145,7 @@ def test_closed_forms_on_gpu(variant, n):
     assert np.all(y[4] == 0)                                           # zeros stay exactly zero
 
 
-@pytest.mark.parametrize("variant,n", [(1, 256), (1, 4096), (1, 8192), (2, 1 << 16), (2, 1 << 17), (3, 1 << 20), (5, 1 << 16),
+@pytest.mark.parametrize("variant,n", [(1, 256), (1, 4096), (1, 8192), (1, 1 << 14), (2, 1 << 16), (2, 1 << 17), (3, 1 << 20), (5, 1 << 16),
                                        (5, 1 << 20)])
 def test_batch_position_bit_identity(variant, n):
     # a record's result does not depend on the batch around it
@@ -241,12 +241,13 @@ def test_cluster_sizes(cs, n):
 
 @pytest.mark.parametrize("impl", [1, 2])
 @pytest.mark.parametrize("b", [1, 3, 449])
-def test_single_implementations(impl, b):
+@pytest.mark.parametrize("n", [1 << 13, 1 << 14])
+def test_single_implementations(impl, b, n):
     # 2^13: k_rows (impl 1) and k_rows_tma (impl 2, the default: records staged by
-    # bulk copies, two compute groups over three stages); 449 records = three or
-    # more per persistent CTA, so every stage and both groups are reused
-    n = 1 << 13
-    x = synth.random_records(61 + impl + b, n, 0, b)
+    # bulk copies, two compute groups over three stages); 2^14: k_rows and
+    # k_rows_tma2 (head staged apart, tail in the exchange buffer); 449 records =
+    # three or more per persistent CTA, so every stage / buffer is refilled
+    x = synth.random_records(61 + impl + b + n, n, 0, b)
     check(x, bf.FFT_FORWARD, bf.VARIANT_SINGLE, impl=impl)
     check(x, bf.FFT_INVERSE, bf.VARIANT_SINGLE, impl=impl)
     y_out, _ = gpu_run(x, bf.FFT_FORWARD, bf.VARIANT_SINGLE, impl=impl)
@@ -256,7 +257,7 @@ def test_single_implementations(impl, b):
 
 def test_single_impl_rejected():
     with pytest.raises(bf.FFTError) as ei:
-        bf.Plan(4096, 1, bf.FFT_FORWARD, bf.VARIANT_SINGLE, impl=2)   # k_rows_tma only at 2^13
+        bf.Plan(4096, 1, bf.FFT_FORWARD, bf.VARIANT_SINGLE, impl=2)   # staged kernels only at 2^13, 2^14
     assert ei.value.code == 1
     with pytest.raises(bf.FFTError) as ei:
         bf.Plan(8192, 1, bf.FFT_FORWARD, bf.VARIANT_SINGLE, impl=3)
@@ -315,8 +316,9 @@ def test_plan_options_rejected():
 
 
 def test_auto_variant_choice():
-    # AUTO picks the single-pass kernel up to 2^13 and the pipelined four-step above
-    for n, want in ((2, "single"), (4096, "single"), (8192, "single"), (1 << 14, "pipe"), (1 << 16, "pipe"),
+    # AUTO picks the single-pass kernels up to 2^14 and the pipelined four-step above
+    for n, want in ((2, "single"), (4096, "single"), (8192, "single"), (1 << 14, "single"), (1 << 15, "pipe"),
+                    (1 << 16, "pipe"),
                     (1 << 22, "pipe")):
         with bf.Plan(n, 2) as p:
             info = p.info()

@@ -66,7 +66,8 @@ def test_r2c_forward_matches_oracle(n):
 
 # 64..1024: partners by warp shuffle at T = 2..32 threads per record; 2048..8192:
 # through shared memory; 2^14: the staged kernel (k_rows_tma); longer: two kernels
-@pytest.mark.parametrize("n", [4, 8, 64, 256, 512, 1024, 2048, 4096, 8192, 1 << 14, 1 << 16, 1 << 20, 1 << 23])
+@pytest.mark.parametrize("n", [4, 8, 64, 256, 512, 1024, 2048, 4096, 8192, 1 << 14, 1 << 15, 1 << 16, 1 << 20,
+                               1 << 23])
 def test_c2r_inverse_matches_oracle(n):
     b = 2 if n >= (1 << 21) else 5
     x = real_records(2000 + n, n, b)
@@ -84,11 +85,12 @@ def test_c2r_inverse_matches_oracle(n):
 
 
 @pytest.mark.parametrize("direction", [-1, 1])
-def test_real_staged_kernel_reuses_stages(direction):
-    # 2^14 reals on k_rows_tma: 449 records = three or more per persistent CTA, so
-    # every stage is refilled and both groups alternate (R2C split through the
-    # stage; C2R merge from the natural-order stage)
-    n, b = 1 << 14, 449
+@pytest.mark.parametrize("n", [1 << 14, 1 << 15])
+def test_real_staged_kernel_reuses_stages(direction, n):
+    # 2^14 reals on k_rows_tma, 2^15 on k_rows_tma2: 449 records = three or more
+    # per persistent CTA, so every stage / buffer is refilled (R2C split through
+    # the exchange buffer; C2R merge from the natural-order staged record)
+    b = 449
     x = real_records(3000 + n, n, b)
     full = oracle.records_c64(x.astype(np.complex64), oracle.FORWARD)
     if direction == bf.FFT_FORWARD:

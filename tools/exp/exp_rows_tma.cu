@@ -4,6 +4,10 @@
 #include <vector>
 using namespace bfft;
 struct Cfg { const void* fn; int threads; size_t smem; int L, pp; const char* name; int kind; };
+template <int L, int PP, int YL> static Cfg mk2(const char* name) {
+    using CF = RowsTma2Cfg<L, PP, YL>;
+    return Cfg{(const void*)&k_rows_tma2<L, false, PP, YL>, CF::NT, CF::SMEM, L, PP, name, 1};
+}
 template <int L, int PP, int NGRP, int NST> static Cfg mk(const char* name) {
     using CF = RowsTmaCfg<L, PP, NGRP, NST>;
     return Cfg{(const void*)&k_rows_tma<L, false, PP, NGRP, NST>, CF::NT, CF::SMEM, L, PP, name, 1};
@@ -22,10 +26,14 @@ static Cfg table(int i) {
         case 6: return mk<4096, 16, 1, 2>("tma 2^12 p16 g1 s2");
         case 7: return mk<4096, 32, 1, 2>("tma 2^12 p32 g1 s2");
         case 8: return mk<8192, 16, 1, 3>("tma 2^13 p16 g1 s3");
+        case 9: return mkr<16384, 32, 1>("k_rows 2^14");
+        case 10: return mk2<16384, 32, 10240>("tma2 2^14 head 10240");
+        case 11: return mk2<16384, 32, 8192>("tma2 2^14 head 8192");
+        case 12: return mk2<16384, 32, 11264>("tma2 2^14 head 11264");
         default: return Cfg{nullptr};
     }
 }
-extern "C" int exp_ncfg() { return 9; }
+extern "C" int exp_ncfg() { return 13; }
 extern "C" const char* exp_name(int i) { return table(i).name; }
 extern "C" int exp_L(int i) { return table(i).L; }
 extern "C" int exp_pp(int i) { return table(i).pp; }
