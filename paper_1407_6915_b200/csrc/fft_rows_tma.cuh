@@ -246,27 +246,37 @@ k_rows_tma2(const float2* __restrict__ in, float2* __restrict__ out, int64_t nre
         fft_engine<L, PP>(v, t, X, [](int e) { return RowLayout::at(e); }, tab, bar);
         float2* dst = out + r * L + t;
         if constexpr (REAL == 1) {
-            // X[k] = E + W_n^k O, E = (Z[k] + conj Z[L-k]) / 2, O = (Z[k] - conj Z[L-k]) / (2i); out[0] = (X[0], X[L])
+            // X[k] = E + W_n^k O, E = (Z[k] + conj Z[L-k]) / 2, O = (Z[k] - conj Z[L-k]) / (2i); out[0] = (X[0], X[L]).
+            // The partner of k = t + qT is element P-1-q of thread T-t (P-q of thread 0 itself): exchanged
+            // in two halves through X[0, L/2), so X's tail can be refilled before the split.
+            static_assert(L / 2 <= YL, "the split exchange stays below the tail");
+            fence_proxy_async_smem();
             __syncthreads();   // the engine's last exchange has been read
-#pragma unroll
-            for (int q = 0; q < P; ++q) X[RowLayout::at(t + q * T)] = v[q];
-            __syncthreads();
-#pragma unroll
-            for (int q = 0; q < P; ++q) {
-                const float2 a = v[q], c = X[RowLayout::at((L - (t + q * T)) & (L - 1))];
+            if (t < 32 && more) load(X + YL, r + G, YL, L, fullX);
+            auto split = [&](int q, float2 c) {
+                const float2 a = v[q];
                 float2 x;
                 if (q == 0 && t == 0) {
                     x = make_float2(a.x + a.y, a.x - a.y);
                 } else {
+                    if (t == 0) c = v[(P - q) & (P - 1)];
                     const float2 e = __fmul2_rn(cadd(a, conjf2(c)), make_float2(0.5f, 0.5f));
                     const float2 o = mul_mi(__fmul2_rn(csub(a, conjf2(c)), make_float2(0.5f, 0.5f)));
                     x = cadd(e, cmul(o, wk(q)));
                 }
                 st_stream(dst + q * T, x);
-            }
-            fence_proxy_async_smem();
+            };
+#pragma unroll
+            for (int q = P / 2; q < P; ++q) X[t + (q - P / 2) * T] = v[q];   // k in [L/2, L)
             __syncthreads();
-            if (t < 32 && more) load(X + YL, r + G, YL, L, fullX);
+#pragma unroll
+            for (int q = 0; q < P / 2; ++q) split(q, X[((T - t) & (T - 1)) + (P / 2 - 1 - q) * T]);
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < P / 2; ++q) X[t + q * T] = v[q];             // k in [0, L/2)
+            __syncthreads();
+#pragma unroll
+            for (int q = P / 2; q < P; ++q) split(q, X[((T - t) & (T - 1)) + (P - 1 - q) * T]);
         } else {
             fence_proxy_async_smem();
             __syncthreads();
