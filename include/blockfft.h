@@ -159,9 +159,10 @@ fft_plan *fft_plan_create_real(int64_t n, int64_t batch, int dir);
  * skips samples), else FFT_E_ARG; n, frames, dir as in fft_plan_create.
  * fft_exec(plan, in, out, stream): in = the signal, (frames-1)*hop + n
  * complex64 samples; out = frames*n complex64; in and out must not overlap.
- * Frames of up to 2^14 points are framed and windowed on load by the
- * single-pass kernel (one launch); longer frames are framed into out by one
- * more kernel and transformed in place.
+ * Frames are framed and windowed on load by the transform kernel itself (one
+ * launch) for any hop up to 2^14 points and an even hop above; an odd hop
+ * above 2^14 points is framed into out by one more kernel and transformed in
+ * place.
  */
 fft_plan *fft_plan_create_stft(int64_t n, int64_t hop, int64_t frames, int dir, const float *window);
 

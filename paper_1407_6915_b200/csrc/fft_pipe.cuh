@@ -416,7 +416,9 @@ __global__ void __launch_bounds__(Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP,
                                   Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP, H>::MINB)
 k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, float2* __restrict__ ring,
         int64_t nrec, int* __restrict__ ctr, int S, int LAG, float scale, const float2* __restrict__ w_hi,
-        const float2* __restrict__ w_lo, int w_lb) {
+        const float2* __restrict__ w_lo, int w_lb, const float* __restrict__ window) {
+    // window: optional per-sample weights w[0..N) applied as the A-tile is read
+    // (STFT frames: tmap_in then strides records by the hop)
     using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP, H>;
     constexpr int LPP = ilog2(PP);
     constexpr int N = CF::N, TA = CF::TA, TB = CF::TB, NTC = CF::NTC, TILE = CF::TILE, RSTRIDE = CF::RSTRIDE;
@@ -636,10 +638,19 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 } else if constexpr (TWM == TW_SPLIT) {
                     w0 = __ldg(w_hi + t * N2 + n2);   // W_N^{n2 t}: in flight during the column FFT
                 }
+                if (window) {
 #pragma unroll
-                for (int q = 0; q < PP; ++q) {
-                    const float2 x = stage[(t + q * TA1) * (H * COLS) + half * COLS + col];
-                    v[q] = INV ? conjf2(x) : x;
+                    for (int q = 0; q < PP; ++q) {
+                        const float w = __ldg(window + (t + q * TA1) * N2 + n2);
+                        const float2 x = stage[(t + q * TA1) * (H * COLS) + half * COLS + col];
+                        v[q] = INV ? make_float2(x.x * w, -x.y * w) : make_float2(x.x * w, x.y * w);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < PP; ++q) {
+                        const float2 x = stage[(t + q * TA1) * (H * COLS) + half * COLS + col];
+                        v[q] = INV ? conjf2(x) : x;
+                    }
                 }
                 if constexpr (H > 1) pair();   // the halves' exchange regions overlap both halves' inputs
                 float2* xch = stage + half * CF::REG_A;

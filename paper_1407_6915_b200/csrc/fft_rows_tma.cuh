@@ -10,7 +10,9 @@
 // idles while both compute (71 % of the roofline, profiles/r01_rows_2p13_minb.txt).
 // Here the next record is already in shared memory when a group finishes.
 //
-// Records are dealt statically: CTA c takes records c, c + grid, ...; task k
+// Records start istride elements apart (L; the hop for STFT frames — even, so
+// the bulk copies stay 16-byte aligned), optionally weighted by window[0..L) on
+// read.  Records are dealt statically: CTA c takes records c, c + grid, ...; task k
 // of a CTA is its k-th record, staged in stage k mod NSTAGE and computed by
 // group k mod NGRP.  There is no producer warp (17 warps would cap registers
 // at 96 per thread: 5 warps on one SM sub-partition): thread 0 stages the first
@@ -51,7 +53,7 @@ struct RowsTmaCfg {
 template <int L, bool INV, int PP, int NGRP, int NSTAGE, int REAL = 0>
 __global__ void __launch_bounds__(RowsTmaCfg<L, PP, NGRP, NSTAGE>::NT, RowsTmaCfg<L, PP, NGRP, NSTAGE>::MINB)
 k_rows_tma(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec, const float2* __restrict__ tw,
-           float scale, RealTw rt) {
+           float scale, RealTw rt, int64_t istride, const float* __restrict__ window) {
     static_assert(REAL == 0 || INV == (REAL == 2), "R2C is forward, C2R inverse");
     using CF = RowsTmaCfg<L, PP, NGRP, NSTAGE>;
     constexpr int T = CF::T, P = CF::S::P, STAGE = CF::STAGE;
@@ -71,7 +73,7 @@ k_rows_tma(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec
         __syncwarp();
         constexpr int CH = L / CF::CHUNKS;
         if (lane < CF::CHUNKS)
-            bulk_g2s_hint(smem_addr(sm + (size_t)s * STAGE + lane * CH), in + r * L + lane * CH, CH * sizeof(float2),
+            bulk_g2s_hint(smem_addr(sm + (size_t)s * STAGE + lane * CH), in + r * istride + lane * CH, CH * sizeof(float2),
                           full0 + 8 * s, pol);
     };
     if (tid == 0) {
@@ -99,7 +101,11 @@ k_rows_tma(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec
             float2 v[P];
 #pragma unroll
             for (int j = 0; j < P; ++j) {
-                const float2 x = stage[t + j * T];
+                float2 x = stage[t + j * T];
+                if (window) {   // STFT frames (istride = the hop): weights applied on read
+                    const float w = __ldg(window + t + j * T);
+                    x = make_float2(x.x * w, x.y * w);
+                }
                 if constexpr (REAL == 2) {
                     // Z[k] = E + i O, E = (X[k] + conj X[L-k]) / 2, O = (X[k] - conj X[L-k]) conj(W_n^k) / 2
                     const int kk = t + j * T;
@@ -177,7 +183,7 @@ struct RowsTma2Cfg {
 template <int L, bool INV, int PP, int YL, int REAL = 0>
 __global__ void __launch_bounds__(RowsTma2Cfg<L, PP, YL>::NT, 1)
 k_rows_tma2(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec, const float2* __restrict__ tw,
-            float scale, RealTw rt) {
+            float scale, RealTw rt, int64_t istride, const float* __restrict__ window) {
     static_assert(REAL == 0 || INV == (REAL == 2), "R2C is forward, C2R inverse");
     using CF = RowsTma2Cfg<L, PP, YL>;
     constexpr int T = CF::T, P = CF::S::P, XS = CF::XS, JY = YL / T;
@@ -195,7 +201,7 @@ k_rows_tma2(const float2* __restrict__ in, float2* __restrict__ out, int64_t nre
         __syncwarp();
         const int ch = (hi - lo) / 4;
         if (lane < 4)
-            bulk_g2s_hint(smem_addr(dst + lane * ch), in + r * L + lo + lane * ch, ch * sizeof(float2), bar, pol);
+            bulk_g2s_hint(smem_addr(dst + lane * ch), in + r * istride + lo + lane * ch, ch * sizeof(float2), bar, pol);
     };
     if (t == 0) {
         mbar_init(fullY, 1);
@@ -221,7 +227,11 @@ k_rows_tma2(const float2* __restrict__ in, float2* __restrict__ out, int64_t nre
         float2 v[P];
 #pragma unroll
         for (int j = 0; j < P; ++j) {
-            const float2 x = j < JY ? Y[t + j * T] : X[t + j * T];
+            float2 x = j < JY ? Y[t + j * T] : X[t + j * T];
+            if (window) {   // STFT frames (istride = the hop): weights applied on read
+                const float w = __ldg(window + t + j * T);
+                x = make_float2(x.x * w, x.y * w);
+            }
             if constexpr (REAL == 2) {
                 // Z[k] = E + i O, E = (X[k] + conj X[L-k]) / 2, O = (X[k] - conj X[L-k]) conj(W_n^k) / 2
                 const int kk = t + j * T;

@@ -79,13 +79,16 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // Records viewed as a 3-D tensor of 8-byte elements [count][n1][n2] (n2
-// fastest); box = {box_cols, box_rows, 1}: one record's column tile.
+// fastest), consecutive records rec_stride elements apart (n1 n2 for records,
+// the hop for STFT frames; a multiple of 2: TMA strides are 16-byte multiples);
+// box = {box_cols, box_rows, 1}: one record's column tile.
 static int make_record_tmap(CUtensorMap* m, const void* base, int64_t count, int n1, int n2, int box_cols,
-                            int box_rows) {
+                            int box_rows, int64_t rec_stride = 0) {
     auto fn = encode_fn();
     if (!fn) return bfft_set_error(FFT_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    if (rec_stride == 0) rec_stride = (int64_t)n1 * n2;
     cuuint64_t dims[3] = {(cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)count};
-    cuuint64_t strides[2] = {(cuuint64_t)n2 * 8, (cuuint64_t)n1 * n2 * 8};
+    cuuint64_t strides[2] = {(cuuint64_t)n2 * 8, (cuuint64_t)rec_stride * 8};
     cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
     cuuint32_t es[3] = {1, 1, 1};
     // L2 promotion 256 B (measured no different from none or 128 B: profiles/r01_tmap_promotion.txt)
@@ -577,6 +580,14 @@ extern "C" fft_plan* fft_plan_create_stft(int64_t n, int64_t hop, int64_t frames
 
 extern "C" void fft_plan_destroy(fft_plan* p) { plan_free(p); }
 
+// STFT frames longer than the single-pass kernels handle are framed (hop-strided
+// tensor map) and windowed as k_pipe2 reads its A-tiles — one launch — when the
+// hop keeps TMA's 16-byte stride alignment; otherwise k_frames frames them first.
+static bool stft_fused(const fft_plan* p) {
+    return p->hop > 0 && p->inner && p->inner->variant == FFT_VARIANT_PIPE && p->inner->pipe_impl == 2 &&
+           p->hop % 2 == 0;
+}
+
 extern "C" int fft_plan_get_info(const fft_plan* p, fft_plan_info* info) {
     if (!p || !info) return bfft_set_error(FFT_E_ARG, "null plan or info pointer");
     if (p->real) {
@@ -593,7 +604,7 @@ extern "C" int fft_plan_get_info(const fft_plan* p, fft_plan_info* info) {
     if (p->hop) {
         int rc = fft_plan_get_info(p->inner, info);
         info->hop = p->hop;
-        if (p->inner->variant != FFT_VARIANT_SINGLE) info->kernels_per_exec += 1;   // + the framing kernel
+        if (p->inner->variant != FFT_VARIANT_SINGLE && !stft_fused(p)) info->kernels_per_exec += 1;   // + k_frames
         return rc;
     }
     info->hop = 0;
@@ -633,12 +644,12 @@ static int launch(const fft_plan* p, const float2* in, float2* out, int64_t coun
             break;
         }
         case FFT_VARIANT_SINGLE: {
-            if (p->kt.fn && istride == n && !window) {
-                // contiguous records: persistent staged kernel, one CTA per SM slot
+            if (p->kt.fn && istride % 2 == 0) {
+                // persistent staged kernel (records, or STFT frames at an even hop: 16-byte aligned copies)
                 const int grid = (int)std::min<int64_t>(count, (int64_t)p->sms * p->occ_t);
                 if (grid > 0)
-                    ((RowTmaFn)p->kt.fn)<<<grid, p->kt.threads, p->kt.smem, st>>>(in, out, count, p->tw_a, p->scale,
-                                                                                   RealTw{nullptr, nullptr, 0});
+                    ((RowTmaFn)p->kt.fn)<<<grid, p->kt.threads, p->kt.smem, st>>>(
+                        in, out, count, p->tw_a, p->scale, RealTw{nullptr, nullptr, 0}, istride, window);
                 break;
             }
             const int64_t groups = (count + p->ka.cols - 1) / p->ka.cols;
@@ -679,11 +690,12 @@ static int launch(const fft_plan* p, const float2* in, float2* out, int64_t coun
             const int grid = p->occ_a * p->sms;
             if (p->pipe_impl >= 2) {
                 CUtensorMap tm;
-                int rc = make_record_tmap(&tm, in, count, p->n1, p->n2, p->ka.cols, p->pipe_boxr);
+                // STFT frames (istride = hop, window): k_pipe2 only (stft_fused)
+                int rc = make_record_tmap(&tm, in, count, p->n1, p->n2, p->ka.cols, p->pipe_boxr, istride);
                 if (rc) return rc;
                 ((Pipe2Fn)p->ka.fn)<<<grid, p->ka.threads, p->ka.smem, st>>>(tm, out, p->d_scratch, count, p->d_ctr,
                                                                             p->pipe_S, p->pipe_LAG, p->scale, p->tw_a,
-                                                                            p->tw_b, p->w_lb);
+                                                                            p->tw_b, p->w_lb, window);
             } else {
                 ((PipeFn)p->ka.fn)<<<grid, p->ka.threads, p->ka.smem, st>>>(in, out, p->d_scratch, count, p->d_ctr,
                                                                            p->pipe_S, p->pipe_LAG, p->scale, p->tw_a,
@@ -737,7 +749,7 @@ extern "C" int fft_exec_range(const fft_plan* p, const void* in, void* out, int6
         // STFT frames: the single-pass kernel frames and windows on load; longer
         // frames are framed into `out` first and transformed in place
         cudaStream_t st = (cudaStream_t)stream;
-        if (p->inner->variant == FFT_VARIANT_SINGLE)
+        if (p->inner->variant == FFT_VARIANT_SINGLE || stft_fused(p))
             return launch(p->inner, (const float2*)in, (float2*)out, count, st, p->hop, p->d_win);
         const int threads = 256;
         const int grid = (int)std::min<int64_t>((count * p->n + threads - 1) / threads, (int64_t)p->sms * 16);
@@ -755,7 +767,8 @@ extern "C" int fft_exec_range(const fft_plan* p, const void* in, void* out, int6
             const int grid = (int)std::min<int64_t>(count, (int64_t)p->sms * p->occ_t);
             if (grid > 0)
                 ((RowTmaFn)p->kt.fn)<<<grid, p->kt.threads, p->kt.smem, st>>>(
-                    (const float2*)in, (float2*)out, count, p->inner->tw_a, p->inner->scale, RealTw{p->tw_a, p->tw_b, p->rt_lb});
+                    (const float2*)in, (float2*)out, count, p->inner->tw_a, p->inner->scale, RealTw{p->tw_a, p->tw_b, p->rt_lb},
+                    h, nullptr);
             cudaError_t e = cudaGetLastError();
             if (e != cudaSuccess) return bfft_set_error(FFT_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
             return FFT_OK;

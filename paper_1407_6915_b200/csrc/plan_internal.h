@@ -31,7 +31,7 @@ struct ClusterChoice {
 
 // kernel signatures, by family (launch casts KernelSet::fn to these)
 using RowFn = void (*)(const float2*, float2*, int64_t, const float2*, float, int64_t, const float*, bfft::RealTw);
-using RowTmaFn = void (*)(const float2*, float2*, int64_t, const float2*, float, bfft::RealTw);
+using RowTmaFn = void (*)(const float2*, float2*, int64_t, const float2*, float, bfft::RealTw, int64_t, const float*);
 using ColFn = void (*)(const float2*, float2*, int64_t, int, const float2*);
 using RowTFn = void (*)(const float2*, float2*, int64_t, int, const float2*, float);
 using ClusterFn = void (*)(const CUtensorMap, float2*, int64_t, const float2*, const float2*, float);
@@ -41,7 +41,7 @@ using PipeFn = void (*)(const float2*, float2*, float2*, int64_t, int*, int, int
                         const float2*, int);
 
 using Pipe2Fn = void (*)(const CUtensorMap, float2*, float2*, int64_t, int*, int, int, float, const float2*,
-                         const float2*, int);
+                         const float2*, int, const float*);
 
 // kern_rows.cu: single-pass row kernel for 2^log2l; four-step column / row kernels
 KernelSet pick_row(int log2l, bool inv);

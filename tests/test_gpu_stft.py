@@ -35,8 +35,8 @@ def hann(n):
 
 
 @pytest.mark.parametrize("n,hop", [(256, 128), (1024, 256), (1024, 768), (1024, 1000), (4096, 1024),
-                                   (8192, 4096), (1 << 14, 4096), (1 << 16, 1 << 15), (1 << 16, 12345),
-                                   (1024, 1500)])
+                                   (8192, 4096), (8192, 4097), (1 << 14, 4096), (1 << 14, 4095), (1 << 16, 1 << 15),
+                                   (1 << 16, 12345), (1024, 1500)])
 @pytest.mark.parametrize("win", [False, True])
 def test_stft_matches_oracle(n, hop, win):
     frames = max(3, min((1 << 21) // n, 257)) | 1
@@ -66,6 +66,27 @@ def test_stft_hop_n_equals_records(n):
         y2 = p.exec(x.view(b, n), torch.empty((b, n), dtype=torch.complex64, device="cuda"))
     torch.cuda.synchronize()
     assert torch.equal(y1, y2)
+
+
+@pytest.mark.parametrize("n,hop,fused", [(1 << 16, 1 << 15, True), (1 << 16, 12346, True), (1 << 16, 12345, False),
+                                         (1 << 15, 1000, True), (1 << 15, 999, False)])
+def test_stft_long_frames_one_kernel(n, hop, fused):
+    # frames longer than 2^14: an even hop is framed by k_pipe2's TMA tensor map
+    # and windowed as its A-tiles are read (one kernel); an odd hop (TMA strides
+    # are 16-byte multiples) goes through k_frames first.  Both vs the oracle.
+    frames = 7
+    length = (frames - 1) * hop + n
+    sig = synth.random_samples(900 + hop, 0, length)
+    w = hann(n)
+    with bf.StftPlan(n, hop, frames, window=w) as p:
+        info = p.info()
+        y = p.exec(torch.from_numpy(sig).cuda())
+    torch.cuda.synchronize()
+    assert info["kernels_per_exec"] == (1 if fused else 2)
+    ref = oracle.records_c64(frames_of(sig, n, hop, frames, w), oracle.FORWARD)
+    err = oracle.rel_l2(y.cpu().numpy(), ref)
+    assert np.all(err <= oracle.tolerance(n)), err.max()
+    assert err.max() <= 2e-6, err.max()
 
 
 def test_stft_errors():

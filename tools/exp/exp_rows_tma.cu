@@ -73,8 +73,9 @@ extern "C" float exp_run(int i, const void* in, void* out, long long nrec, int r
     for (int it = 0; it < reps; ++it) {
         cudaEventRecord(a);
         if (c.kind == 1) {
-            using Fn = void (*)(const float2*, float2*, int64_t, const float2*, float, RealTw);
-            ((Fn)c.fn)<<<occ * 148, c.threads, c.smem>>>((const float2*)in, (float2*)out, nrec, dtw, 1.f, RealTw{});
+            using Fn = void (*)(const float2*, float2*, int64_t, const float2*, float, RealTw, int64_t, const float*);
+            ((Fn)c.fn)<<<occ * 148, c.threads, c.smem>>>((const float2*)in, (float2*)out, nrec, dtw, 1.f, RealTw{}, c.L,
+                                                        nullptr);
         } else {
             using Fn = void (*)(const float2*, float2*, int64_t, const float2*, float, int64_t, const float*, RealTw);
             const int grid = (int)std::min<long long>(nrec, (long long)occ * 148 * 8);
