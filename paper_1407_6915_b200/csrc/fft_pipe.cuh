@@ -410,19 +410,38 @@ struct PipeTask {
 // H*COLS*8-byte DRAM run per row; a B-task H*ROWS ring rows) staged together
 // and computed by H groups, one tile each: groups g = H j .. H j + H - 1 take
 // tasks k = j, j + NGRP / H, ...
+// RS = 1 (real records of n = 2N samples, forward; H = 2): the real split
+// X[k] = E + W_n^k O (E = (Z[k] + conj Z[N-k])/2, O = (Z[k] - conj Z[N-k])/(2i),
+// SURVEY.md §8(f) NEXT-1) is fused into the B-task.  The partner of k = k1 + N1 k2
+// is N - k = (N1 - k1) + N1 (N2 - 1 - k2), so a B-task takes rows k1 = tile*ROWS + c
+// (half 0) and their mirrors N1 - k1 (half 1; the mirror of row 0 is row 0 itself,
+// and row N1/2 — its own mirror — takes that slot), exchanges the transformed rows
+// through the stage and stores the packed half spectrum (X[0] slot = (X[0], X[N])).
 template <int N1, int N2, int COLS, int ROWS, bool INV, int NSTAGE, int PP = 16, int TWM = TW_TREE, int NGRP = 1,
-          int CB = 1, bool PF = false, int H = 1>
+          int CB = 1, bool PF = false, int H = 1, int RS = 0>
 __global__ void __launch_bounds__(Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP, H>::NT,
                                   Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP, H>::MINB)
 k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, float2* __restrict__ ring,
         int64_t nrec, int* __restrict__ ctr, int S, int LAG, float scale, const float2* __restrict__ w_hi,
-        const float2* __restrict__ w_lo, int w_lb, const float* __restrict__ window) {
+        const float2* __restrict__ w_lo, int w_lb, const float* __restrict__ window, RealTw rt) {
     // window: optional per-sample weights w[0..N) applied as the A-tile is read
     // (STFT frames: tmap_in then strides records by the hop)
+    // rt: W_n^k (n = 2N) for RS = 1, else unused
+    static_assert(RS == 0 || (H == 2 && !INV), "the fused real split is forward, over mirrored half tiles");
     using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP, H>;
     constexpr int LPP = ilog2(PP);
     constexpr int N = CF::N, TA = CF::TA, TB = CF::TB, NTC = CF::NTC, TILE = CF::TILE, RSTRIDE = CF::RSTRIDE;
     constexpr int TA1 = Sched<N1, PP>::T, TB2 = Sched<N2, PP>::T;
+    // B-task row of half h, slot c (RS: half 1 holds the mirrors, see above)
+    auto brow = [](int tile, int h, int c) -> int {
+        if constexpr (RS) {
+            if (h == 0) return tile * ROWS + c;
+            const int m = N1 - tile * ROWS - c;
+            return m == N1 ? N1 / 2 : m;
+        } else {
+            return (tile * H + h) * ROWS + c;
+        }
+    };
     extern __shared__ __align__(128) float2 sm[];
     PipeTask* info = reinterpret_cast<PipeTask*>(sm + (size_t)TILE * NSTAGE);
     uint64_t* bars = reinterpret_cast<uint64_t*>(info + NSTAGE);   // full | empty | done | sfree
@@ -558,9 +577,10 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 }
             } else {
                 const int slot = (int)(d.rec % S);
-                const float2* src = ring + (int64_t)slot * N + (int64_t)d.tile * H * ROWS * N2;
+                const float2* src = ring + (int64_t)slot * N;
                 for (int j = lane; j < H * ROWS; j += 32)
-                    bulk_g2s(smem_addr(stage + j * RSTRIDE), src + (int64_t)j * N2, N2 * sizeof(float2), fb);
+                    bulk_g2s(smem_addr(stage + j * RSTRIDE), src + (int64_t)brow(d.tile, j / ROWS, j % ROWS) * N2,
+                             N2 * sizeof(float2), fb);
             }
             ++k;
         }
@@ -692,17 +712,19 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
             } else {
                 // ---------------- B: rows k1 of record r, FFT over n2, -> X[k1 + N1 k2]
                 const int col = gtid % ROWS, t = gtid / ROWS;
-                const int k0 = (d.tile * H + half) * ROWS;
+                const int k1 = brow(d.tile, half, col);
                 const float2* srow = stage + (half * ROWS + col) * RSTRIDE;
                 {   // the tile's ring rows are staged: drop them from L2 (no write-back)
-                    const char* rows = reinterpret_cast<const char*>(ring + (int64_t)slot * N + (int64_t)k0 * N2);
-                    for (int i = gtid; i < ROWS * N2 * 8 / 128; i += NTC) l2_discard128(rows + 128 * i);
+                    constexpr int LPR = N2 * 8 / 128;   // 128-byte lines per row
+                    const char* base = reinterpret_cast<const char*>(ring + (int64_t)slot * N);
+                    for (int i = gtid; i < ROWS * LPR; i += NTC)
+                        l2_discard128(base + ((int64_t)brow(d.tile, half, i / LPR) * N2) * 8 + 128 * (i % LPR));
                 }
                 if constexpr (TWM == TW_SPLIT) {
                     // the W_{N2 PP}^{n2 qa} part, n2 = t + TB2 s, qa = k1 / TA1, applied
                     // as the elements arrive, 8 at a time (a compiler barrier keeps the
                     // loads from all being hoisted: v plus every factor would spill)
-                    const int qa = (k0 + col) / TA1;
+                    const int qa = k1 / TA1;
                     const float2 wb = tw_b0[t * PP + qa];
                     const float2* trow = tw_t + qa * (PP + 1);
 #pragma unroll
@@ -721,15 +743,47 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
 #ifndef BFFT_PIPE_NOCOMPUTE
                 fft_engine<N2, PP>(v, t, xch, [&](int e) { return CF::LayB::at(e, col); }, tabB, bar);
 #endif
+                float2* dst = out + r * N + k1 + (int64_t)t * N1;
+                if constexpr (RS) {
+                    // the real split: both halves' rows through the stage, then X[k] = E + W_n^k O
+                    pair();   // both groups are done with their exchange regions
+                    float2* zrow = stage + (half * ROWS + col) * RSTRIDE;
+#pragma unroll
+                    for (int q = 0; q < PP; ++q) zrow[t + q * TB2] = v[q];
+                    pair();
+                    const bool self = d.tile == 0 && col == 0;   // rows 0 and N1/2: their own mirrors
+                    const float2* prow = self ? zrow : stage + ((1 - half) * ROWS + col) * RSTRIDE;
+                    const float2 a = rt(k1 + N1 * t);            // W_n^{k1 + N1 t}; W_n^{N1 TB2 q} = W_{2PP}^q
+#pragma unroll
+                    for (int q = 0; q < PP; ++q) {
+                        const int k2 = t + q * TB2;
+                        const int pk2 = (self && half == 0) ? ((N2 - k2) & (N2 - 1)) : (N2 - 1 - k2);
+                        const float2 z = v[q], c = prow[pk2];
+                        float2 x;
+                        if (self && half == 0 && k2 == 0) {
+                            x = make_float2(z.x + z.y, z.x - z.y);                     // (X[0], X[N])
+                        } else {
+                            const float2 e = __fmul2_rn(cadd(z, conjf2(c)), make_float2(0.5f, 0.5f));
+                            const float2 o = mul_mi(__fmul2_rn(csub(z, conjf2(c)), make_float2(0.5f, 0.5f)));
+                            x = cadd(e, cmul(o, cmul(a, c_rw64[q * (32 / PP)])));
+                        }
+                        st_stream(dst + (int64_t)q * TB2 * N1, x);
+                    }
+#ifndef BFFT_PIPE_NOFENCE
+                    fence_proxy_async_smem();
+#endif
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(sfree0 + 8 * s);
+                } else {
 #ifndef BFFT_PIPE_NOFENCE
                 fence_proxy_async_smem();   // last generic access of the stage: before its next bulk refill
 #endif
                 __syncwarp();
                 if (lane == 0) mbar_arrive(sfree0 + 8 * s);   // the producer may refill the stage now
-                float2* dst = out + r * N + k0 + col + (int64_t)t * N1;
 #pragma unroll
                 for (int q = 0; q < PP; ++q)
                     st_stream(dst + (int64_t)q * TB2 * N1, INV ? scale_conj(v[q], scale) : v[q]);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(done0 + 8 * s);

@@ -87,7 +87,8 @@ template <int N1, int N2, int COLS, int ROWS, bool INV, int NS, int G, int PP = 
 __global__ void __launch_bounds__(Pipe3Cfg<N1, N2, COLS, ROWS, NS, G, PP>::NT, Pipe3Cfg<N1, N2, COLS, ROWS, NS, G, PP>::MINB)
 k_pipe3(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, float2* __restrict__ ring,
         int64_t nrec, int* __restrict__ ctr, int S, int LAG, float scale, const float2* __restrict__ w_hi,
-        const float2* __restrict__ w_lo, int w_lb, const float* __restrict__ /*window: k_pipe2 only, pass null*/) {
+        const float2* __restrict__ w_lo, int w_lb, const float* __restrict__ /*window: k_pipe2 only, pass null*/,
+        RealTw /*k_pipe2 only*/) {
     using CF = Pipe3Cfg<N1, N2, COLS, ROWS, NS, G, PP>;
     constexpr int LPP = ilog2(PP);
     constexpr int N = CF::N, TA = CF::TA, TB = CF::TB, NTC = CF::NTC, TILE = CF::TILE, RSTRIDE = CF::RSTRIDE;

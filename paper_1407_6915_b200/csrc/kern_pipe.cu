@@ -25,6 +25,36 @@ static PipeChoice pipe2_kernel(bool inv) {
     ch.k.smem = pipe2_smem<N1, N2, COLS, ROWS, NSTAGE, PP, TWM, NGRP>();
     return ch;
 }
+// k_pipe2 with the real split fused (RS = 1: forward real records of 2 N1 N2
+// samples; two groups per task over mirrored half tiles, one CTA per SM)
+template <int N1, int N2, int COLS, int ROWS, int PP = 32>
+static PipeChoice pipe2_real_kernel() {
+    constexpr int NSTAGE = 3, NGRP = 4, H = 2;
+    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP, H>;
+    PipeChoice ch;
+    ch.n1 = N1;
+    ch.n2 = N2;
+    ch.cols = H * COLS;   // a task's columns / rows (tensor-map box, tasks per round)
+    ch.rows = H * ROWS;
+    ch.impl = 2;
+    ch.stages = NSTAGE;
+    ch.boxr = CF::BOXR;
+    ch.k.fn = (const void*)&k_pipe2<N1, N2, COLS, ROWS, false, NSTAGE, PP, TW_SPLIT, NGRP, 2, false, H, 1>;
+    ch.twm = TW_SPLIT;
+    ch.pp = PP;
+    ch.k.threads = CF::NT;
+    ch.k.smem = pipe2_smem<N1, N2, COLS, ROWS, NSTAGE, PP, TW_SPLIT, NGRP, H>();
+    return ch;
+}
+PipeChoice pick_pipe_real(int log2n) {
+    switch (log2n) {   // complex length N = n / 2
+        case 15: return pipe2_real_kernel<256, 128, 16, 32>();
+        case 16: return pipe2_real_kernel<256, 256, 16, 16>();
+        case 17: return pipe2_real_kernel<512, 256, 8, 16>();
+        case 18: return pipe2_real_kernel<512, 512, 8, 8>();
+        default: return PipeChoice{};
+    }
+}
 template <int N1, int N2, int COLS, int ROWS> static PipeChoice pipe_kernel(bool inv) {
     using CF = PipeCfg<N1, N2, COLS, ROWS>;
     PipeChoice ch;

@@ -170,6 +170,7 @@ struct fft_plan {
     int grid_a = 0, grid_b = 0;       // persistent/capped grid sizes (per full batch)
     int occ_a = 0, occ_b = 0;
     int real = 0;                     // 1: real records (fft_plan_create_real), n reals each
+    int real_split = 0;               // inner plan of a real plan: k_pipe2 with the split fused (RS)
     int64_t hop = 0;                  // > 0: STFT frames every `hop` samples (fft_plan_create_stft)
     float* d_win = nullptr;           // STFT: optional window, n floats
     fft_plan* inner = nullptr;        // real: the n/2-point complex plan; STFT: the frames' plan
@@ -245,7 +246,7 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, const fft_p
         stockham_table(ch.n1, ta, ch.pp);
         stockham_table(ch.n2, tb, ch.pp);
     } else if (variant == FFT_VARIANT_PIPE) {
-        PipeChoice ch = pick_pipe(p->log2n, inv, o.impl, o.config);
+        PipeChoice ch = p->real_split ? pick_pipe_real(p->log2n) : pick_pipe(p->log2n, inv, o.impl, o.config);
         if (!ch.k.fn) return bfft_set_error(FFT_E_SIZE, "unsupported transform size for pipelined variant: %lld", (long long)n);
         p->ka = ch.k;
         p->n1 = ch.n1;
@@ -351,7 +352,7 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, const fft_p
         p->occ_a = std::max(p->occ_a, 1);
         const int resident = p->occ_a * p->sms;
         const int per_round = p->n2 / p->ka.cols + p->n1 / p->kb.cols;
-        PipeChoice ch = pick_pipe(p->log2n, inv, o.impl, o.config);
+        PipeChoice ch = p->real_split ? pick_pipe_real(p->log2n) : pick_pipe(p->log2n, inv, o.impl, o.config);
         // B-tasks of record r are issued LAG rounds after its A-tasks, and an
         // A-task reuses the ring slot of record r - S, whose B-tasks were
         // issued S - LAG rounds earlier.  Both gaps must exceed the tasks a
@@ -475,7 +476,23 @@ extern "C" fft_plan* fft_plan_create_real(int64_t n, int64_t batch, int dir) {
     p->batch = batch;
     p->dir = dir;
     p->log2n = ilog2((int)(n >> 1)) + 1;
-    p->inner = fft_plan_create_opts(n / 2, batch, dir, nullptr);
+    // forward records of 2^16..2^19 samples: k_pipe2 with the split fused (one
+    // launch); other sizes: the complex n/2-point plan (+ k_real_split above 2^15)
+    if (dir == FFT_FORWARD && pick_pipe_real(ilog2((int)(n / 2))).k.fn) {
+        fft_plan* q = new (std::nothrow) fft_plan();
+        if (!q) {
+            bfft_set_error(FFT_E_NOMEM, "out of host memory");
+            return fail();
+        }
+        q->real_split = 1;
+        fft_plan_opts o{};
+        o.variant = FFT_VARIANT_PIPE;
+        o.impl = 2;
+        p->inner = q;
+        if (plan_init(q, n / 2, batch, dir, o) != FFT_OK) return fail();
+    } else {
+        p->inner = fft_plan_create_opts(n / 2, batch, dir, nullptr);
+    }
     if (!p->inner) return fail();
     p->device = p->inner->device;
     p->sms = p->inner->sms;
@@ -594,7 +611,8 @@ extern "C" int fft_plan_get_info(const fft_plan* p, fft_plan_info* info) {
         int rc = fft_plan_get_info(p->inner, info);
         info->n = p->n;
         info->dir = p->dir;
-        if (!p->ka.fn && !p->kt.fn) info->kernels_per_exec += 1;  // + the split / merge kernel (fused up to 2^15)
+        if (!p->ka.fn && !p->kt.fn && !p->inner->real_split)
+            info->kernels_per_exec += 1;   // + the split / merge kernel (fused up to 2^15, and forward to 2^19)
         info->table_bytes += (int64_t)p->tab_bytes;
         info->real = 1;
         info->hop = 0;
@@ -631,7 +649,7 @@ extern "C" int fft_plan_get_info(const fft_plan* p, fft_plan_info* info) {
 
 // ------------------------------------------------------------ exec
 static int launch(const fft_plan* p, const float2* in, float2* out, int64_t count, cudaStream_t st,
-                  int64_t istride = 0, const float* window = nullptr) {
+                  int64_t istride = 0, const float* window = nullptr, RealTw rt = RealTw{nullptr, nullptr, 0}) {
     const int64_t n = p->n;
     if (istride == 0) istride = n;
     switch (p->variant) {
@@ -695,7 +713,7 @@ static int launch(const fft_plan* p, const float2* in, float2* out, int64_t coun
                 if (rc) return rc;
                 ((Pipe2Fn)p->ka.fn)<<<grid, p->ka.threads, p->ka.smem, st>>>(tm, out, p->d_scratch, count, p->d_ctr,
                                                                             p->pipe_S, p->pipe_LAG, p->scale, p->tw_a,
-                                                                            p->tw_b, p->w_lb, window);
+                                                                            p->tw_b, p->w_lb, window, rt);
             } else {
                 ((PipeFn)p->ka.fn)<<<grid, p->ka.threads, p->ka.smem, st>>>(in, out, p->d_scratch, count, p->d_ctr,
                                                                            p->pipe_S, p->pipe_LAG, p->scale, p->tw_a,
@@ -783,6 +801,9 @@ extern "C" int fft_exec_range(const fft_plan* p, const void* in, void* out, int6
             if (e != cudaSuccess) return bfft_set_error(FFT_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
             return FFT_OK;
         }
+        if (p->inner->real_split)   // k_pipe2 with the split fused
+            return launch(p->inner, (const float2*)in, (float2*)out, count, st, 0, nullptr,
+                          RealTw{p->tw_a, p->tw_b, p->rt_lb});
         if (p->dir == FFT_FORWARD) {
             int rc = launch(p->inner, (const float2*)in, (float2*)out, count, st);
             if (rc) return rc;

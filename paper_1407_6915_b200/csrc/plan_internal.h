@@ -41,7 +41,7 @@ using PipeFn = void (*)(const float2*, float2*, float2*, int64_t, int*, int, int
                         const float2*, int);
 
 using Pipe2Fn = void (*)(const CUtensorMap, float2*, float2*, int64_t, int*, int, int, float, const float2*,
-                         const float2*, int, const float*);
+                         const float2*, int, const float*, bfft::RealTw);
 
 // kern_rows.cu: single-pass row kernel for 2^log2l; four-step column / row kernels
 KernelSet pick_row(int log2l, bool inv);
@@ -58,6 +58,9 @@ KernelSet pick_fs_row(int log2l, bool inv);
 ClusterChoice pick_cluster(int log2n, int want_c, bool inv, int impl);
 // kern_pipe.cu: pipelined four-step (k_pipe / k_pipe2, or k_pipe3 through pick_pipe3)
 PipeChoice pick_pipe(int log2n, bool inv, int impl, int config);
+// kern_pipe.cu: k_pipe2 with the forward real split fused (complex length
+// 2^log2n; empty choice where none is built)
+PipeChoice pick_pipe_real(int log2n);
 // each kernel unit's copy of the constant twiddles (same contents as plan.cu's); 0 on success
 int rows_upload_const(const float2* host, size_t count);
 int cluster_upload_const(const float2* host, size_t count);

@@ -109,6 +109,36 @@ def test_real_staged_kernel_reuses_stages(direction, n):
     assert err.max() <= 2e-6, err.max()
 
 
+@pytest.mark.parametrize("n", [1 << 16, 1 << 17, 1 << 18, 1 << 19])
+def test_r2c_fused_pipelined_wraps_ring(n):
+    # forward records of 2^16..2^19 samples: k_pipe2 with the split fused into its
+    # B-tasks (mirrored half tiles).  A batch of 2S + 3 records wraps the L2 ring
+    # twice; sampled records (first, last, reused slots, seeded picks) vs the oracle.
+    with bf.RealPlan(n, 1) as p:
+        info = p.info()
+    assert info["kernels_per_exec"] == 1 and info["variant_name"] == "pipe", info
+    s = info["ring_records"]
+    b = 2 * s + 3
+    x = torch.empty((b, n), dtype=torch.float32, device="cuda")
+    torch.manual_seed(n)
+    x.uniform_(-1, 1)
+    with bf.RealPlan(n, b) as p:
+        y = p.exec(x)
+    torch.cuda.synchronize()
+    rows = sorted({0, 1, s - 1, s, s + 1, 2 * s, 2 * s + 1, b - 1})
+    xs = x[rows].cpu().numpy()
+    ref = packed_from_full(oracle.records_c64(xs.astype(np.complex64), oracle.FORWARD))
+    err = oracle.rel_l2(y[rows].cpu().numpy(), ref)
+    assert np.all(err <= oracle.tolerance(n)), err.max()
+    assert err.max() <= 2e-6, err.max()
+    # batch independence: the same records alone
+    with bf.RealPlan(n, 1) as p1:
+        for i, r in enumerate(rows):
+            y1 = p1.exec(x[r:r + 1].contiguous())
+            torch.cuda.synchronize()
+            assert torch.equal(y1[0], y[r]), r
+
+
 def test_r2c_closed_forms_and_in_place():
     n = 1024
     j = np.arange(n)

@@ -71,7 +71,7 @@ CASES = [
 def test_stress_build_bit_identical(n, b, o, both):
     lib = stress_lib()
     if b is None:
-        with bf.Plan(n, 1, **o) as p:
+        with bf.Plan(n, 1, bf.FFT_FORWARD, bf.VARIANT_PIPE, **o) as p:
             b = 2 * p.info()["ring_records"] + 3
     x = torch.empty((b, n), dtype=torch.complex64, device="cuda")
     sg.fill_random(x, 99 + n)

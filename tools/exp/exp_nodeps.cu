@@ -33,7 +33,7 @@ extern "C" float exp_run(const void* in, void* out, void* ring, int* ctr, long l
         cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
         cudaEventRecord(a);
         fn<<<occ * 148, CF::NT, CF::SMEM>>>(tm, (float2*)out, (float2*)ring, nrec, ctr, S, LAG, 1.f,
-                                            (const float2*)hi, (const float2*)lo, lb, nullptr);
+                                            (const float2*)hi, (const float2*)lo, lb, nullptr, RealTw{});
         cudaEventRecord(b); cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b);
         if (ms < best) best = ms;

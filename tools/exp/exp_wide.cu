@@ -93,7 +93,7 @@ extern "C" float exp_run(int i, const void* in, void* out, void* ring, int* ctr,
         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     using Fn = void (*)(const CUtensorMap, float2*, float2*, int64_t, int*, int, int, float, const float2*,
-                        const float2*, int, const float*);
+                        const float2*, int, const float*, RealTw);
     Fn fn = (Fn)c.fn;
     float best = 1e9f;
     cudaEvent_t a, b;
@@ -103,7 +103,7 @@ extern "C" float exp_run(int i, const void* in, void* out, void* ring, int* ctr,
         cudaMemsetAsync(ctr, 0, sizeof(int) * (1 + 2 * S));
         cudaEventRecord(a);
         fn<<<occ * 148, c.threads, c.smem>>>(tm, (float2*)out, (float2*)ring, nrec, ctr, S, LAG, 1.f,
-                                             (const float2*)hi, (const float2*)lo, lb, nullptr);
+                                             (const float2*)hi, (const float2*)lo, lb, nullptr, RealTw{});
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms;
