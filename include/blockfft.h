@@ -140,9 +140,8 @@ fft_plan *fft_plan_create_opts(int64_t n, int64_t batch, int dir, const fft_plan
  *     (1/n) sum_k X[k] exp(+2 pi i jk/n) over the Hermitian-extended X.
  * The record is read as the n/2-point complex signal x[2m] + i x[2m+1] (the
  * same bytes), transformed by an n/2-point complex plan, and split / merged
- * with W_n^k: inside the transform kernel (one launch) up to n = 2^15, and
- * forward up to 2^19 (k_pipe2 over mirrored row tiles); otherwise by one more
- * kernel (csrc/real.cu).
+ * with W_n^k inside the transform kernel (one launch) up to n = 2^19; longer
+ * records by one more kernel (csrc/real.cu).
  * Input and output are both 4n bytes per record, so in place works and a
  * streamed real file moves half the bytes of its complex64 promotion.
  * fft_exec on such a plan: 16-byte aligned pointers to batch*4n bytes.

@@ -194,6 +194,7 @@ struct RealTw {
     const float2* hi;
     const float2* lo;
     int lb;
+    const float2* src = nullptr;   // k_pipe2 RS = 2: the packed half spectra (partner reads)
     __device__ __forceinline__ float2 operator()(int k) const {
         return cmul(__ldg(hi + (k >> lb)), __ldg(lo + (k & ((1 << lb) - 1))));
     }

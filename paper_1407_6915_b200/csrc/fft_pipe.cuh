@@ -417,6 +417,8 @@ struct PipeTask {
 // (half 0) and their mirrors N1 - k1 (half 1; the mirror of row 0 is row 0 itself,
 // and row N1/2 — its own mirror — takes that slot), exchanges the transformed rows
 // through the stage and stores the packed half spectrum (X[0] slot = (X[0], X[N])).
+// RS = 2 (inverse): the C2R merge is fused into the A-task's read (rt.src holds
+// the packed half spectra for the partner reads).
 template <int N1, int N2, int COLS, int ROWS, bool INV, int NSTAGE, int PP = 16, int TWM = TW_TREE, int NGRP = 1,
           int CB = 1, bool PF = false, int H = 1, int RS = 0>
 __global__ void __launch_bounds__(Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP, H>::NT,
@@ -427,14 +429,15 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
     // window: optional per-sample weights w[0..N) applied as the A-tile is read
     // (STFT frames: tmap_in then strides records by the hop)
     // rt: W_n^k (n = 2N) for RS = 1, else unused
-    static_assert(RS == 0 || (H == 2 && !INV), "the fused real split is forward, over mirrored half tiles");
+    static_assert(RS == 0 || (RS == 1 && H == 2 && !INV) || (RS == 2 && INV),
+                  "fused real split: forward over mirrored half tiles (1), merge on load: inverse (2)");
     using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP, H>;
     constexpr int LPP = ilog2(PP);
     constexpr int N = CF::N, TA = CF::TA, TB = CF::TB, NTC = CF::NTC, TILE = CF::TILE, RSTRIDE = CF::RSTRIDE;
     constexpr int TA1 = Sched<N1, PP>::T, TB2 = Sched<N2, PP>::T;
     // B-task row of half h, slot c (RS: half 1 holds the mirrors, see above)
     auto brow = [](int tile, int h, int c) -> int {
-        if constexpr (RS) {
+        if constexpr (RS == 1) {
             if (h == 0) return tile * ROWS + c;
             const int m = N1 - tile * ROWS - c;
             return m == N1 ? N1 / 2 : m;
@@ -658,7 +661,33 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 } else if constexpr (TWM == TW_SPLIT) {
                     w0 = __ldg(w_hi + t * N2 + n2);   // W_N^{n2 t}: in flight during the column FFT
                 }
-                if (window) {
+                if constexpr (RS == 2) {
+                    // C2R merge on load: Z[k] = E + i O, E = (X[k] + conj X[N-k]) / 2,
+                    // O = (X[k] - conj X[N-k]) conj(W_n^k) / 2 for k = n1 N2 + n2; the
+                    // partner N - k = (N1 - 1 - n1) N2 + (N2 - n2) (n2 > 0) or
+                    // (N1 - n1) N2 (n2 = 0) is read from L2 / HBM (the mirrored
+                    // column tile's own A-task stages it too).  W_n^k = W_n^{n2 + N2 t}
+                    // W_{2PP}^q for n1 = t + TA1 q.
+                    const float2* xr = rt.src + r * N;
+                    const float2 a = rt((int)n2 + N2 * t);
+#pragma unroll
+                    for (int q = 0; q < PP; ++q) {
+                        const int n1 = t + q * TA1;
+                        const float2 x = stage[n1 * (H * COLS) + half * COLS + col];
+                        const int pk = n2 ? (N1 - 1 - n1) * N2 + (N2 - n2) : ((N1 - n1) & (N1 - 1)) * N2;
+                        float2 z;
+                        if (n2 == 0 && n1 == 0) {
+                            z = make_float2(0.5f * (x.x + x.y), 0.5f * (x.x - x.y));   // (E[0], O[0])
+                        } else {
+                            const float2 y = __ldg(xr + pk);
+                            const float2 e = __fmul2_rn(cadd(x, conjf2(y)), make_float2(0.5f, 0.5f));
+                            const float2 o = cmul(__fmul2_rn(csub(x, conjf2(y)), make_float2(0.5f, 0.5f)),
+                                                  conjf2(cmul(a, c_rw64[q * (32 / PP)])));
+                            z = cadd(e, mul_pi(o));
+                        }
+                        v[q] = conjf2(z);   // INV
+                    }
+                } else if (window) {
 #pragma unroll
                     for (int q = 0; q < PP; ++q) {
                         const float w = __ldg(window + (t + q * TA1) * N2 + n2);
@@ -744,7 +773,7 @@ k_pipe2(const __grid_constant__ CUtensorMap tmap_in, float2* __restrict__ out, f
                 fft_engine<N2, PP>(v, t, xch, [&](int e) { return CF::LayB::at(e, col); }, tabB, bar);
 #endif
                 float2* dst = out + r * N + k1 + (int64_t)t * N1;
-                if constexpr (RS) {
+                if constexpr (RS == 1) {
                     // the real split: both halves' rows through the stage, then X[k] = E + W_n^k O
                     pair();   // both groups are done with their exchange regions
                     float2* zrow = stage + (half * ROWS + col) * RSTRIDE;

@@ -170,7 +170,7 @@ struct fft_plan {
     int grid_a = 0, grid_b = 0;       // persistent/capped grid sizes (per full batch)
     int occ_a = 0, occ_b = 0;
     int real = 0;                     // 1: real records (fft_plan_create_real), n reals each
-    int real_split = 0;               // inner plan of a real plan: k_pipe2 with the split fused (RS)
+    int real_split = 0;               // inner plan of a real plan: k_pipe2 with the split (1) or merge (2) fused
     int64_t hop = 0;                  // > 0: STFT frames every `hop` samples (fft_plan_create_stft)
     float* d_win = nullptr;           // STFT: optional window, n floats
     fft_plan* inner = nullptr;        // real: the n/2-point complex plan; STFT: the frames' plan
@@ -246,7 +246,9 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, const fft_p
         stockham_table(ch.n1, ta, ch.pp);
         stockham_table(ch.n2, tb, ch.pp);
     } else if (variant == FFT_VARIANT_PIPE) {
-        PipeChoice ch = p->real_split ? pick_pipe_real(p->log2n) : pick_pipe(p->log2n, inv, o.impl, o.config);
+        PipeChoice ch = p->real_split == 1   ? pick_pipe_real(p->log2n)
+                         : p->real_split == 2 ? pick_pipe_real_inv(p->log2n)
+                                              : pick_pipe(p->log2n, inv, o.impl, o.config);
         if (!ch.k.fn) return bfft_set_error(FFT_E_SIZE, "unsupported transform size for pipelined variant: %lld", (long long)n);
         p->ka = ch.k;
         p->n1 = ch.n1;
@@ -352,7 +354,9 @@ static int plan_init(fft_plan* p, int64_t n, int64_t batch, int dir, const fft_p
         p->occ_a = std::max(p->occ_a, 1);
         const int resident = p->occ_a * p->sms;
         const int per_round = p->n2 / p->ka.cols + p->n1 / p->kb.cols;
-        PipeChoice ch = p->real_split ? pick_pipe_real(p->log2n) : pick_pipe(p->log2n, inv, o.impl, o.config);
+        PipeChoice ch = p->real_split == 1   ? pick_pipe_real(p->log2n)
+                         : p->real_split == 2 ? pick_pipe_real_inv(p->log2n)
+                                              : pick_pipe(p->log2n, inv, o.impl, o.config);
         // B-tasks of record r are issued LAG rounds after its A-tasks, and an
         // A-task reuses the ring slot of record r - S, whose B-tasks were
         // issued S - LAG rounds earlier.  Both gaps must exceed the tasks a
@@ -476,15 +480,20 @@ extern "C" fft_plan* fft_plan_create_real(int64_t n, int64_t batch, int dir) {
     p->batch = batch;
     p->dir = dir;
     p->log2n = ilog2((int)(n >> 1)) + 1;
-    // forward records of 2^16..2^19 samples: k_pipe2 with the split fused (one
-    // launch); other sizes: the complex n/2-point plan (+ k_real_split above 2^15)
-    if (dir == FFT_FORWARD && pick_pipe_real(ilog2((int)(n / 2))).k.fn) {
+    // 2^16..2^19 samples: k_pipe2 with the split (forward) or the merge (inverse)
+    // fused — one launch (measured: the fused merge loses to two kernels above
+    // 2^19, where its partner reads miss L2; profiles/r02_real_bench_shfl.txt);
+    // other sizes: the complex n/2-point plan (+ k_real_split above 2^15)
+    const bool fuse = n >= (1 << 16) && n <= (1 << 19);
+    const int rs = !fuse ? 0 : dir == FFT_FORWARD ? (pick_pipe_real(ilog2((int)(n / 2))).k.fn ? 1 : 0)
+                                                  : (pick_pipe_real_inv(ilog2((int)(n / 2))).k.fn ? 2 : 0);
+    if (rs) {
         fft_plan* q = new (std::nothrow) fft_plan();
         if (!q) {
             bfft_set_error(FFT_E_NOMEM, "out of host memory");
             return fail();
         }
-        q->real_split = 1;
+        q->real_split = rs;
         fft_plan_opts o{};
         o.variant = FFT_VARIANT_PIPE;
         o.impl = 2;
@@ -801,9 +810,9 @@ extern "C" int fft_exec_range(const fft_plan* p, const void* in, void* out, int6
             if (e != cudaSuccess) return bfft_set_error(FFT_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
             return FFT_OK;
         }
-        if (p->inner->real_split)   // k_pipe2 with the split fused
+        if (p->inner->real_split)   // k_pipe2 with the split / merge fused (merge: partners read from in)
             return launch(p->inner, (const float2*)in, (float2*)out, count, st, 0, nullptr,
-                          RealTw{p->tw_a, p->tw_b, p->rt_lb});
+                          RealTw{p->tw_a, p->tw_b, p->rt_lb, (const float2*)in});
         if (p->dir == FFT_FORWARD) {
             int rc = launch(p->inner, (const float2*)in, (float2*)out, count, st);
             if (rc) return rc;

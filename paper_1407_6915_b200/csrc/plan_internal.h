@@ -61,6 +61,8 @@ PipeChoice pick_pipe(int log2n, bool inv, int impl, int config);
 // kern_pipe.cu: k_pipe2 with the forward real split fused (complex length
 // 2^log2n; empty choice where none is built)
 PipeChoice pick_pipe_real(int log2n);
+// kern_pipe.cu: k_pipe2 with the inverse real merge fused into the A-task read
+PipeChoice pick_pipe_real_inv(int log2n);
 // each kernel unit's copy of the constant twiddles (same contents as plan.cu's); 0 on success
 int rows_upload_const(const float2* host, size_t count);
 int cluster_upload_const(const float2* host, size_t count);

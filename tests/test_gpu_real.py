@@ -139,6 +139,35 @@ def test_r2c_fused_pipelined_wraps_ring(n):
             assert torch.equal(y1[0], y[r]), r
 
 
+@pytest.mark.parametrize("n", [1 << 16, 1 << 17, 1 << 19])
+def test_c2r_fused_pipelined_wraps_ring(n):
+    # inverse records of 2^16..2^19 samples: k_pipe2 with the C2R merge fused into
+    # its A-task reads (partners from the packed spectra in HBM / L2).  2S + 3
+    # records wrap the ring twice; sampled records vs the oracle's inverse of the
+    # Hermitian-extended spectrum, and vs the same records alone.
+    with bf.RealPlan(n, 1, bf.FFT_INVERSE) as p:
+        info = p.info()
+    assert info["kernels_per_exec"] == 1 and info["variant_name"] == "pipe", info
+    s = info["ring_records"]
+    b = min(2 * s + 3, max(3, (1 << 29) // n))   # at most 2 GiB of spectra
+    P = torch.empty((b, n // 2), dtype=torch.complex64, device="cuda")
+    torch.manual_seed(n + 1)
+    P.view(torch.float32).uniform_(-1, 1)
+    with bf.RealPlan(n, b, bf.FFT_INVERSE) as p:
+        z = p.exec(P)
+    torch.cuda.synchronize()
+    rows = sorted({0, 1, min(b - 1, s), min(b - 1, s + 1), min(b - 1, 2 * s + 1), b - 1})
+    Ph = P[rows].cpu().numpy()
+    ref = oracle.records_c64(full_from_packed(Ph.astype(np.complex128)).astype(np.complex64), oracle.INVERSE)
+    err = oracle.rel_l2(z[rows].cpu().numpy().astype(np.complex128), ref.real.astype(np.complex128))
+    assert np.all(err <= oracle.tolerance(n)), err.max()
+    with bf.RealPlan(n, 1, bf.FFT_INVERSE) as p1:
+        for r in rows:
+            z1 = p1.exec(P[r:r + 1].contiguous())
+            torch.cuda.synchronize()
+            assert torch.equal(z1[0], z[r]), r
+
+
 def test_r2c_closed_forms_and_in_place():
     n = 1024
     j = np.arange(n)

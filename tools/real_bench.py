@@ -22,7 +22,9 @@ rows = []
 floats = int(a.gib * 2 ** 30) // 4
 buf = torch.rand(floats, device="cuda") * 2 - 1
 out = torch.empty(floats // 2, dtype=torch.complex64, device="cuda")
-for k in (10, 12, 13, 14, 15, 16, 18, 20):
+import os
+KS = [int(v) for v in os.environ.get("REAL_BENCH_K", "10,12,13,14,15,16,18,20").split(",")]
+for k in KS:
     n = 1 << k
     b = floats // n
     x, y = buf[: b * n].view(b, n), out[: b * n // 2].view(b, n // 2)
