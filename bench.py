@@ -272,7 +272,7 @@ def main():
     kernels_per_exec = info["kernels_per_exec"]
     achieved = alg_bytes / avg_launch_s / 1e9
     kname = {"cluster": "k_cluster", "single": "k_rows", "fourstep": "k_fs", "identity": "k_copy",
-             "pipe": "k_pipe"}[info["variant_name"]]
+             "pipe": "k_pipe2"}[info["variant_name"]]   # the default pipelined kernel (impl 2)
     traffic, traffic_src = ncu_traffic(kname, n, batch)
 
     # end to end through the public C ABI (fft_exec_host) with HOST buffers:
