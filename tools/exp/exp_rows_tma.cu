@@ -30,10 +30,20 @@ static Cfg table(int i) {
         case 10: return mk2<16384, 32, 10240>("tma2 2^14 head 10240");
         case 11: return mk2<16384, 32, 8192>("tma2 2^14 head 8192");
         case 12: return mk2<16384, 32, 11264>("tma2 2^14 head 11264");
+        case 13: return mkr<512, 16, 8>("k_rows 2^9 p16 (default)");
+        case 14: return mkr<512, 32, 16>("k_rows 2^9 p32");
+        case 15: return mkr<1024, 16, 4>("k_rows 2^10 p16 (default)");
+        case 16: return mkr<1024, 32, 8>("k_rows 2^10 p32");
+        case 17: return mkr<2048, 16, 2>("k_rows 2^11 p16 (default)");
+        case 18: return mkr<2048, 32, 4>("k_rows 2^11 p32");
+        case 19: return mkr<4096, 32, 2>("k_rows 2^12 p32");
+        case 20: return mkr<256, 16, 16>("k_rows 2^8 p16 (default)");
+        case 21: return mk<4096, 32, 2, 3>("tma 2^12 p32 g2 s3");
+        case 22: return mk<4096, 16, 1, 3>("tma 2^12 p16 g1 s3");
         default: return Cfg{nullptr};
     }
 }
-extern "C" int exp_ncfg() { return 13; }
+extern "C" int exp_ncfg() { return 23; }
 extern "C" const char* exp_name(int i) { return table(i).name; }
 extern "C" int exp_L(int i) { return table(i).L; }
 extern "C" int exp_pp(int i) { return table(i).pp; }
