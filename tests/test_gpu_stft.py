@@ -69,7 +69,8 @@ def test_stft_hop_n_equals_records(n):
 
 
 @pytest.mark.parametrize("n,hop,fused", [(1 << 16, 1 << 15, True), (1 << 16, 12346, True), (1 << 16, 12345, False),
-                                         (1 << 15, 1000, True), (1 << 15, 999, False)])
+                                         (1 << 15, 1000, True), (1 << 15, 999, False), (1 << 15, 40000, True),
+                                         (1 << 20, 1 << 19, True)])
 def test_stft_long_frames_one_kernel(n, hop, fused):
     # frames longer than 2^14: an even hop is framed by k_pipe2's TMA tensor map
     # and windowed as its A-tiles are read (one kernel); an odd hop (TMA strides
