@@ -32,10 +32,15 @@ static Cfg table(int i) {
         case 11: return mk<16, 16, 4, 32, TW_SPLIT, 4, 1, false, 2>("c16 h2 s4 g4");
         case 12: return mk<8, 8, 3, 32, TW_SPLIT, 4, 1, false, 2>("c8 h2 s3 g4");
         case 13: return mk<8, 8, 3, 32, TW_SPLIT, 8, 1, false, 4>("c8 h4 s3 g8");
+        case 14: return mk<16, 16, 5, 32, TW_SPLIT, 4, 4>("c16 s5 g4 cb4");
+        case 15: return mk<16, 16, 6, 32, TW_SPLIT, 4, 4>("c16 s6 g4 cb4");
+        case 16: return mk<16, 16, 6, 32, TW_SPLIT, 4, 2>("c16 s6 g4 cb2");
+        case 17: return mk<16, 16, 6, 32, TW_SPLIT, 3, 4>("c16 s6 g3 cb4");
+        case 18: return mk<16, 16, 3, 32, TW_SPLIT, 2, 2>("c16 s3 g2 cb2");
         default: return Cfg{nullptr, 0, 0, 0, 0, 0, 0, 0, 0, nullptr, 1, 1};
     }
 }
-extern "C" int exp_ncfg() { return 14; }
+extern "C" int exp_ncfg() { return 19; }
 // the constant-memory Stockham twiddles of this translation unit (same table as plan.cu builds)
 static void stockham_table(int L, std::vector<float2>& out, int P) {
     out.clear();
