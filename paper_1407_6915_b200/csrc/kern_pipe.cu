@@ -56,7 +56,7 @@ static PipeChoice pipe2_real_inv_kernel() {
 }
 PipeChoice pick_pipe_real_inv(int log2n) {
     switch (log2n) {   // complex length N = n / 2; the configurations pick_pipe ships
-        case 15: return pipe2_real_inv_kernel<256, 128, 16, 32, 3, 32, 2>();
+        case 15: return pipe2_real_inv_kernel<128, 256, 32, 16, 3, 32, 2>();
         case 16: return pipe2_real_inv_kernel<256, 256, 16, 16, 3, 32, 2>();
         case 17: return pipe2_real_inv_kernel<512, 256, 8, 16, 3, 32, 2>();
         case 18: return pipe2_real_inv_kernel<512, 512, 16, 16, 3, 32, 2>();
@@ -116,7 +116,9 @@ PipeChoice pick_pipe(int log2n, bool inv, int impl, int config) {
         // two compute groups per CTA over three stages (two CTAs per SM: 16 compute warps)
         switch (log2n) {
             case 14: return pipe2_kernel<128, 128, 16, 16, 3, 16, TW_SPLIT, 2>(inv);
-            case 15: return pipe2_kernel<256, 128, 16, 32, 3, 32, TW_SPLIT, 2>(inv);
+            // 2^15 as 128 x 256: 32-wide A-tiles (256-byte DRAM runs), 63.4 % vs 60.1 % for
+            // 256 x 128 with 16 x 32 tiles (profiles/r02_pipe2_factorisations.txt)
+            case 15: return pipe2_kernel<128, 256, 32, 16, 3, 32, TW_SPLIT, 2>(inv);
             case 16: return pipe2_kernel<256, 256, 16, 16, 3, 32, TW_SPLIT, 2>(inv);
             case 17: return pipe2_kernel<512, 256, 8, 16, 3, 32, TW_SPLIT, 2>(inv);
             case 18: return pipe2_kernel<512, 512, 8, 8, 3, 32, TW_TREE, 2>(inv);

@@ -1,0 +1,108 @@
+// Experiment (not product code): k_pipe2 factorisations N = N1 x N2 and tile
+// shapes at 2^15, 2^17, 2^18 (generalised from exp_wide.cu).
+#include "../../paper_1407_6915_b200/csrc/fft_pipe.cuh"
+#include <cudaTypedefs.h>
+#include <cmath>
+#include <vector>
+using namespace bfft;
+
+struct Cfg { const void* fn; int threads; size_t smem; int cols, rows, stages, twm, boxr, pp; const char* name; int cb; int h; int n1, n2; };
+
+template <int N1, int N2, int COLS, int ROWS, int NST, int PP, int TWM, int NGRP = 1, int CB = 1>
+static Cfg mk(const char* name) {
+    using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NST, PP, NGRP>;
+    return Cfg{(const void*)&k_pipe2<N1, N2, COLS, ROWS, false, NST, PP, TWM, NGRP, CB>, CF::NT,
+               pipe2_smem<N1, N2, COLS, ROWS, NST, PP, TWM, NGRP>(), COLS, ROWS, NST, TWM, CF::BOXR, PP, name, CB, 1,
+               N1, N2};
+}
+static Cfg table(int i) {
+    switch (i) {
+        case 0: return mk<256, 128, 16, 32, 3, 32, TW_SPLIT, 2>("2^15 256x128 c16 r32 s3 g2 (default)");
+        case 1: return mk<128, 256, 32, 16, 3, 32, TW_SPLIT, 2>("2^15 128x256 c32 r16 s3 g2");
+        case 2: return mk<512, 256, 8, 16, 3, 32, TW_SPLIT, 2>("2^17 512x256 c8 r16 s3 g2 (default)");
+        case 3: return mk<256, 512, 16, 8, 3, 32, TW_SPLIT, 2>("2^17 256x512 c16 r8 s3 g2");
+        case 4: return mk<512, 512, 16, 16, 3, 32, TW_SPLIT, 2>("2^18 512x512 c16 r16 s3 g2 (default, 64K)");
+        case 5: return mk<128, 256, 32, 16, 2, 32, TW_SPLIT, 1>("2^15 128x256 c32 r16 s2 g1");
+        default: return Cfg{nullptr};
+    }
+}
+extern "C" int exp_ncfg() { return 6; }
+extern "C" int exp_n1(int i) { return table(i).n1; }
+extern "C" int exp_n2(int i) { return table(i).n2; }
+// the constant-memory Stockham twiddles of this translation unit (same table as plan.cu builds)
+static void stockham_table(int L, std::vector<float2>& out, int P) {
+    out.clear();
+    if (L <= P) return;
+    const int K = ilog2(L), KP = ilog2(P);
+    const int R0 = (K % KP) ? (1 << (K % KP)) : P;
+    const int npass = (K % KP) ? 1 + K / KP : K / KP;
+    for (int p = 1; p < npass; ++p) {
+        const int Ns = R0 * (1 << (KP * (p - 1)));
+        const int M = P * Ns;
+        for (int q = 1; q < P; ++q)
+            for (int jj = 0; jj < Ns; ++jj) {
+                const double ang = -2.0 * M_PI * (double)((long long)jj * q) / (double)M;
+                out.push_back(make_float2((float)cos(ang), (float)sin(ang)));
+            }
+    }
+}
+extern "C" int exp_upload_tw() {
+    std::vector<float2> all, one;
+    for (int pp = 16; pp <= 32; pp *= 2)
+        for (int l = CTW_MIN_L; l <= ctw_max_l(pp); l *= 2) {
+            stockham_table(l, one, pp);
+            all.insert(all.end(), one.begin(), one.end());
+        }
+    if ((int)all.size() != CTW_TOTAL) return 1;
+    return cudaMemcpyToSymbol(c_tw, all.data(), all.size() * sizeof(float2)) != cudaSuccess;
+}
+extern "C" const char* exp_name(int i) { return table(i).name; }
+extern "C" int exp_twm(int i) { return table(i).twm; }
+extern "C" int exp_pp(int i) { return table(i).pp; }
+// returns the best of `reps` launch times in ms (or -1); S/LAG as the plan sizes them
+extern "C" float exp_run(int i, const void* in, void* out, void* ring, int* ctr, long long nrec, int maxS,
+                         const void* hi, const void* lo, int lb, int reps, int* sOut, int* occOut) {
+    Cfg c = table(i);
+    if (!c.fn) return -1.f;
+    cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, c.fn, c.threads, c.smem);
+    if (occ < 1) return -2.f;
+    const int resident = occ * 148, per_round = c.n2 / (c.cols * c.h) + c.n1 / (c.rows * c.h);
+    const long long inflight = (long long)resident * (c.stages + c.cb);
+    const long long rounds = (inflight + per_round - 1) / per_round;
+    int LAG = (int)(3 * rounds / 2 + 1);
+    int S = (int)(LAG + 2 * rounds + 1);
+    if (S > maxS) S = maxS;
+    *sOut = S; *occOut = occ;
+    void* p = nullptr; cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    auto enc = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    CUtensorMap tm;
+    cuuint64_t dims[3] = {(cuuint64_t)c.n2, (cuuint64_t)c.n1, (cuuint64_t)nrec};
+    cuuint64_t strides[2] = {(cuuint64_t)c.n2 * 8, (cuuint64_t)c.n1 * c.n2 * 8};
+    cuuint32_t box[3] = {(cuuint32_t)(c.cols * c.h), (cuuint32_t)c.boxr, 1}, es[3] = {1, 1, 1};
+    enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(in), dims, strides, box, es,
+        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    using Fn = void (*)(const CUtensorMap, float2*, float2*, int64_t, int*, int, int, float, const float2*,
+                        const float2*, int, const float*, RealTw);
+    Fn fn = (Fn)c.fn;
+    float best = 1e9f;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (int it = 0; it < reps; ++it) {
+        cudaMemsetAsync(ctr, 0, sizeof(int) * (1 + 2 * S));
+        cudaEventRecord(a);
+        fn<<<occ * 148, c.threads, c.smem>>>(tm, (float2*)out, (float2*)ring, nrec, ctr, S, LAG, 1.f,
+                                             (const float2*)hi, (const float2*)lo, lb, nullptr, RealTw{});
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (cudaGetLastError() != cudaSuccess) return -3.f;
+        if (ms < best) best = ms;
+    }
+    return best;
+}
