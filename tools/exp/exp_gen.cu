@@ -23,10 +23,14 @@ static Cfg table(int i) {
         case 3: return mk<256, 512, 16, 8, 3, 32, TW_SPLIT, 2>("2^17 256x512 c16 r8 s3 g2");
         case 4: return mk<512, 512, 16, 16, 3, 32, TW_SPLIT, 2>("2^18 512x512 c16 r16 s3 g2 (default, 64K)");
         case 5: return mk<128, 256, 32, 16, 2, 32, TW_SPLIT, 1>("2^15 128x256 c32 r16 s2 g1");
+        case 6: return mk<256, 256, 16, 16, 3, 32, TW_SPLIT, 2>("2^16 256x256 c16 r16 s3 g2 (default)");
+        case 7: return mk<128, 512, 32, 8, 3, 32, TW_SPLIT, 2>("2^16 128x512 c32 r8 s3 g2");
+        case 8: return mk<512, 128, 8, 32, 3, 32, TW_SPLIT, 2>("2^16 512x128 c8 r32 s3 g2");
+        case 9: return mk<128, 128, 32, 32, 3, 32, TW_SPLIT, 2>("2^14 128x128 c32 r32 s3 g2");
         default: return Cfg{nullptr};
     }
 }
-extern "C" int exp_ncfg() { return 6; }
+extern "C" int exp_ncfg() { return 10; }
 extern "C" int exp_n1(int i) { return table(i).n1; }
 extern "C" int exp_n2(int i) { return table(i).n2; }
 // the constant-memory Stockham twiddles of this translation unit (same table as plan.cu builds)
