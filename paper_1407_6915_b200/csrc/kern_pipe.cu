@@ -120,7 +120,10 @@ PipeChoice pick_pipe(int log2n, bool inv, int impl, int config) {
             // 256 x 128 with 16 x 32 tiles (profiles/r02_pipe2_factorisations.txt)
             case 15: return pipe2_kernel<128, 256, 32, 16, 3, 32, TW_SPLIT, 2>(inv);
             case 16: return pipe2_kernel<256, 256, 16, 16, 3, 32, TW_SPLIT, 2>(inv);
-            case 17: return pipe2_kernel<512, 256, 8, 16, 3, 32, TW_SPLIT, 2>(inv);
+            // 2^17 as 256 x 512: 16-wide A-tiles (128-byte runs), twiddles from the full
+            // [k1][n2] table (the split tables' shared memory would cost the second CTA):
+            // 61.3 % vs 57.6 % for 512 x 256 (profiles/r02_pipe2_factorisations.txt)
+            case 17: return pipe2_kernel<256, 512, 16, 8, 3, 32, TW_TABLE, 2>(inv);
             case 18: return pipe2_kernel<512, 512, 8, 8, 3, 32, TW_TREE, 2>(inv);
             case 19: return pipe2_kernel<1024, 512, 8, 16, 3, 32, TW_SPLIT, 2>(inv);
             case 20: return pipe2_kernel<1024, 1024, 8, 8, 3, 32, TW_SPLIT, 2>(inv);

@@ -27,10 +27,24 @@ static Cfg table(int i) {
         case 7: return mk<128, 512, 32, 8, 3, 32, TW_SPLIT, 2>("2^16 128x512 c32 r8 s3 g2");
         case 8: return mk<512, 128, 8, 32, 3, 32, TW_SPLIT, 2>("2^16 512x128 c8 r32 s3 g2");
         case 9: return mk<128, 128, 32, 32, 3, 32, TW_SPLIT, 2>("2^14 128x128 c32 r32 s3 g2");
+        case 10: return mk<256, 512, 16, 8, 3, 32, TW_TREE, 2>("2^17 256x512 c16 r8 s3 g2 tree");
+        case 11: return mk<256, 512, 16, 8, 3, 32, TW_TABLE, 2>("2^17 256x512 c16 r8 s3 g2 table");
+        case 12: return mk<512, 256, 8, 16, 3, 32, TW_TREE, 2>("2^17 512x256 c8 r16 s3 g2 tree");
+        case 13: return mk<128, 512, 32, 8, 3, 32, TW_TREE, 2>("2^16 128x512 c32 r8 s3 g2 tree");
+        case 14: return mk<512, 512, 8, 8, 3, 32, TW_TABLE, 2>("2^18 512x512 c8 r8 s3 g2 table");
+        case 15: return mk<512, 512, 16, 16, 3, 32, TW_TABLE, 2>("2^18 512x512 c16 r16 s3 g2 table");
+        case 16: return mk<1024, 512, 8, 16, 3, 32, TW_TABLE, 2>("2^19 1024x512 c8 r16 s3 g2 table");
+        case 17: return mk<1024, 512, 8, 16, 3, 32, TW_SPLIT, 2>("2^19 1024x512 c8 r16 s3 g2 (default)");
+        case 18: return mk<1024, 1024, 8, 8, 3, 32, TW_TABLE, 2>("2^20 1024x1024 c8 r8 s3 g2 table");
+        case 19: return mk<1024, 1024, 8, 8, 3, 32, TW_SPLIT, 2>("2^20 1024x1024 c8 r8 s3 g2 (default)");
+        case 20: return mk<512, 512, 8, 8, 3, 32, TW_TREE, 2>("2^18 512x512 c8 r8 s3 g2 tree");
+        case 21: return mk<512, 1024, 16, 8, 3, 32, TW_TABLE, 2>("2^19 512x1024 c16 r8 s3 g2 table");
+        case 22: return mk<256, 256, 16, 16, 3, 32, TW_TABLE, 2>("2^16 256x256 c16 r16 s3 g2 table");
+        case 23: return mk<128, 256, 32, 16, 3, 32, TW_TABLE, 2>("2^15 128x256 c32 r16 s3 g2 table");
         default: return Cfg{nullptr};
     }
 }
-extern "C" int exp_ncfg() { return 10; }
+extern "C" int exp_ncfg() { return 24; }
 extern "C" int exp_n1(int i) { return table(i).n1; }
 extern "C" int exp_n2(int i) { return table(i).n2; }
 // the constant-memory Stockham twiddles of this translation unit (same table as plan.cu builds)

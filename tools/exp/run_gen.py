@@ -21,15 +21,23 @@ for i in cfgs:
     x = torch.randn((b, n), dtype=torch.complex64, device="cuda"); y = torch.empty_like(x)
     ref = torch.fft.fft(x[:4].to(torch.complex128))
     ta1, tb2 = n1 // pp, n2 // pp
-    wa = tw(ar(ta1).view(-1, 1) * ar(n2).view(1, -1), n)
-    wb = torch.cat([tw(ar(tb2).view(-1, 1) * ar(pp).view(1, -1), n2 * pp).flatten(),
-                    tw(ar(pp).view(-1, 1) * ar(pp).view(1, -1), pp * pp).flatten()])
+    twm = lib.exp_twm(i)
+    lbv = 0
+    if twm == 2:     # TW_SPLIT
+        wa = tw(ar(ta1).view(-1, 1) * ar(n2).view(1, -1), n)
+        wb = torch.cat([tw(ar(tb2).view(-1, 1) * ar(pp).view(1, -1), n2 * pp).flatten(),
+                        tw(ar(pp).view(-1, 1) * ar(pp).view(1, -1), pp * pp).flatten()])
+    elif twm == 1:   # TW_TABLE: [k1][n2]
+        wa = tw(ar(n1).view(-1, 1) * ar(n2).view(1, -1), n); wb = wa
+    else:            # TW_TREE: two-level W_N (hi, lo)
+        lbv = (n.bit_length() - 1) // 2
+        wa = tw(ar(n >> lbv) * (1 << lbv), n); wb = tw(ar(1 << lbv), n)
     maxS = (96 << 20) // (8 * n)
     ring = torch.empty((maxS, n), dtype=torch.complex64, device="cuda")
     ctr = torch.zeros(2 + 2 * maxS, dtype=torch.int32, device="cuda")
     S, occ = i32(), i32()
     ms = lib.exp_run(i, x.data_ptr(), y.data_ptr(), ring.data_ptr(), ctr.data_ptr(), b, maxS,
-                     wa.data_ptr(), wb.data_ptr(), 0, 5, ctypes.byref(S), ctypes.byref(occ))
+                     wa.data_ptr(), wb.data_ptr(), lbv, 5, ctypes.byref(S), ctypes.byref(occ))
     torch.cuda.synchronize()
     err = float(((y[:4].to(torch.complex128) - ref).abs().pow(2).sum(1).sqrt() / ref.abs().pow(2).sum(1).sqrt()).max())
     gbs = 16.0 * n * b / (ms * 1e-3) / 1e9 if ms > 0 else 0
