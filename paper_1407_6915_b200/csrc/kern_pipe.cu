@@ -6,7 +6,7 @@
 
 using namespace bfft;
 
-template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP = 16, int TWM = TW_SPLIT, int NGRP = 1>
+template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP = 16, int TWM = TW_SPLIT, int NGRP = 1, int CB = 1>
 static PipeChoice pipe2_kernel(bool inv) {
     using CF = Pipe2Cfg<N1, N2, COLS, ROWS, NSTAGE, PP, NGRP>;
     PipeChoice ch;
@@ -17,8 +17,8 @@ static PipeChoice pipe2_kernel(bool inv) {
     ch.impl = 2;
     ch.stages = NSTAGE;
     ch.boxr = CF::BOXR;
-    ch.k.fn = inv ? (const void*)&k_pipe2<N1, N2, COLS, ROWS, true, NSTAGE, PP, TWM, NGRP>
-                  : (const void*)&k_pipe2<N1, N2, COLS, ROWS, false, NSTAGE, PP, TWM, NGRP>;
+    ch.k.fn = inv ? (const void*)&k_pipe2<N1, N2, COLS, ROWS, true, NSTAGE, PP, TWM, NGRP, CB>
+                  : (const void*)&k_pipe2<N1, N2, COLS, ROWS, false, NSTAGE, PP, TWM, NGRP, CB>;
     ch.twm = TWM;
     ch.pp = PP;
     ch.k.threads = CF::NT;
@@ -108,7 +108,8 @@ PipeChoice pick_pipe(int log2n, bool inv, int impl, int config) {
         // two groups, three 64 KiB stages of 16-wide tiles (one CTA per SM)
         switch (log2n) {
             case 17: return pipe2_kernel<512, 256, 16, 32, 3, 32, TW_SPLIT, 2>(inv);
-            case 18: return pipe2_kernel<512, 512, 16, 16, 3, 32, TW_SPLIT, 2>(inv);
+            // claims batched two at a time: 60.3 -> 61.8 % (profiles/r02_pipe2_factorisations.txt)
+            case 18: return pipe2_kernel<512, 512, 16, 16, 3, 32, TW_SPLIT, 2, 2>(inv);
             default: return PipeChoice{};
         }
     }
@@ -123,9 +124,11 @@ PipeChoice pick_pipe(int log2n, bool inv, int impl, int config) {
             // 2^17 as 256 x 512: 16-wide A-tiles (128-byte runs), twiddles from the full
             // [k1][n2] table (the split tables' shared memory would cost the second CTA):
             // 61.3 % vs 57.6 % for 512 x 256 (profiles/r02_pipe2_factorisations.txt)
-            case 17: return pipe2_kernel<256, 512, 16, 8, 3, 32, TW_TABLE, 2>(inv);
+            case 17: return pipe2_kernel<256, 512, 16, 8, 3, 32, TW_TABLE, 2, 2>(inv);
             case 18: return pipe2_kernel<512, 512, 8, 8, 3, 32, TW_TREE, 2>(inv);
-            case 19: return pipe2_kernel<1024, 512, 8, 16, 3, 32, TW_SPLIT, 2>(inv);
+            // 2^19 as 512 x 1024: 16-wide A-tiles (128-byte runs) — 60 % vs 56.7 % for
+            // 1024 x 512 with 8-wide tiles (profiles/r02_pipe2_factorisations.txt)
+            case 19: return pipe2_kernel<512, 1024, 16, 8, 3, 32, TW_SPLIT, 2>(inv);
             case 20: return pipe2_kernel<1024, 1024, 8, 8, 3, 32, TW_SPLIT, 2>(inv);
             default: return PipeChoice{};
         }

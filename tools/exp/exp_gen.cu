@@ -41,10 +41,25 @@ static Cfg table(int i) {
         case 21: return mk<512, 1024, 16, 8, 3, 32, TW_TABLE, 2>("2^19 512x1024 c16 r8 s3 g2 table");
         case 22: return mk<256, 256, 16, 16, 3, 32, TW_TABLE, 2>("2^16 256x256 c16 r16 s3 g2 table");
         case 23: return mk<128, 256, 32, 16, 3, 32, TW_TABLE, 2>("2^15 128x256 c32 r16 s3 g2 table");
+        case 24: return mk<1024, 1024, 8, 8, 3, 32, TW_TREE, 2>("2^20 1024x1024 c8 r8 s3 g2 tree");
+        case 25: return mk<1024, 1024, 8, 8, 3, 32, TW_SPLIT, 2, 2>("2^20 1024x1024 c8 r8 s3 g2 cb2");
+        case 26: return mk<1024, 1024, 8, 8, 2, 32, TW_SPLIT, 1>("2^20 1024x1024 c8 r8 s2 g1");
+        case 27: return mk<1024, 512, 8, 16, 3, 32, TW_TREE, 2>("2^19 1024x512 c8 r16 s3 g2 tree");
+        case 28: return mk<1024, 512, 8, 16, 3, 32, TW_SPLIT, 2, 2>("2^19 1024x512 c8 r16 s3 g2 cb2");
+        case 29: return mk<512, 1024, 16, 8, 3, 32, TW_SPLIT, 2>("2^19 512x1024 c16 r8 s3 g2");
+        case 30: return mk<512, 1024, 16, 8, 3, 32, TW_TREE, 2>("2^19 512x1024 c16 r8 s3 g2 tree");
+        case 31: return mk<512, 512, 16, 16, 3, 32, TW_TREE, 2>("2^18 512x512 c16 r16 s3 g2 tree");
+        case 32: return mk<512, 512, 16, 16, 3, 32, TW_SPLIT, 2, 2>("2^18 512x512 c16 r16 s3 g2 cb2");
+        case 33: return mk<256, 1024, 16, 4, 3, 32, TW_TABLE, 2>("2^18 256x1024 c16 r4 s3 g2 table");
+        case 34: return mk<512, 1024, 16, 8, 3, 32, TW_SPLIT, 2, 2>("2^19 512x1024 c16 r8 s3 g2 cb2");
+        case 35: return mk<512, 512, 16, 16, 3, 32, TW_SPLIT, 2, 4>("2^18 512x512 c16 r16 s3 g2 cb4");
+        case 36: return mk<256, 512, 16, 8, 3, 32, TW_TABLE, 2, 2>("2^17 256x512 c16 r8 s3 g2 table cb2");
+        case 37: return mk<128, 256, 32, 16, 3, 32, TW_SPLIT, 2, 2>("2^15 128x256 c32 r16 s3 g2 cb2");
+        case 38: return mk<512, 1024, 16, 8, 3, 32, TW_SPLIT, 2, 4>("2^19 512x1024 c16 r8 s3 g2 cb4");
         default: return Cfg{nullptr};
     }
 }
-extern "C" int exp_ncfg() { return 24; }
+extern "C" int exp_ncfg() { return 39; }
 extern "C" int exp_n1(int i) { return table(i).n1; }
 extern "C" int exp_n2(int i) { return table(i).n2; }
 // the constant-memory Stockham twiddles of this translation unit (same table as plan.cu builds)
