@@ -56,10 +56,17 @@ static Cfg table(int i) {
         case 36: return mk<256, 512, 16, 8, 3, 32, TW_TABLE, 2, 2>("2^17 256x512 c16 r8 s3 g2 table cb2");
         case 37: return mk<128, 256, 32, 16, 3, 32, TW_SPLIT, 2, 2>("2^15 128x256 c32 r16 s3 g2 cb2");
         case 38: return mk<512, 1024, 16, 8, 3, 32, TW_SPLIT, 2, 4>("2^19 512x1024 c16 r8 s3 g2 cb4");
+        case 39: return mk<2048, 1024, 4, 8, 2, 16, TW_SPLIT, 1>("2^21 2048x1024 c4 r8 s2 g1 (default)");
+        case 40: return mk<2048, 1024, 4, 8, 3, 16, TW_SPLIT, 1>("2^21 2048x1024 c4 r8 s3 g1");
+        case 41: return mk<2048, 1024, 4, 8, 2, 16, TW_SPLIT, 1, 2>("2^21 2048x1024 c4 r8 s2 g1 cb2");
+        case 42: return mk<2048, 1024, 4, 8, 3, 16, TW_SPLIT, 1, 2>("2^21 2048x1024 c4 r8 s3 g1 cb2");
+        case 43: return mk<2048, 2048, 4, 4, 2, 16, TW_SPLIT, 1>("2^22 2048x2048 c4 r4 s2 g1 (default)");
+        case 44: return mk<2048, 2048, 4, 4, 3, 16, TW_SPLIT, 1, 2>("2^22 2048x2048 c4 r4 s3 g1 cb2");
+        case 45: return mk<2048, 1024, 2, 4, 3, 16, TW_SPLIT, 2>("2^21 2048x1024 c2 r4 s3 g2");
         default: return Cfg{nullptr};
     }
 }
-extern "C" int exp_ncfg() { return 39; }
+extern "C" int exp_ncfg() { return 46; }
 extern "C" int exp_n1(int i) { return table(i).n1; }
 extern "C" int exp_n2(int i) { return table(i).n2; }
 // the constant-memory Stockham twiddles of this translation unit (same table as plan.cu builds)
