@@ -40,10 +40,13 @@ static Cfg table(int i) {
         case 20: return mkr<256, 16, 16>("k_rows 2^8 p16 (default)");
         case 21: return mk<4096, 32, 2, 3>("tma 2^12 p32 g2 s3");
         case 22: return mk<4096, 16, 1, 3>("tma 2^12 p16 g1 s3");
+        case 23: return mk2<16384, 16, 10240>("tma2 2^14 p16 head 10240");
+        case 24: return mk2<8192, 32, 4096>("tma2 2^13 p32 head 4096");
+        case 25: return mk2<8192, 16, 4096>("tma2 2^13 p16 head 4096");
         default: return Cfg{nullptr};
     }
 }
-extern "C" int exp_ncfg() { return 23; }
+extern "C" int exp_ncfg() { return 26; }
 extern "C" const char* exp_name(int i) { return table(i).name; }
 extern "C" int exp_L(int i) { return table(i).L; }
 extern "C" int exp_pp(int i) { return table(i).pp; }
