@@ -65,9 +65,9 @@ PipeChoice pick_pipe_real_inv(int log2n) {
 }
 PipeChoice pick_pipe_real(int log2n) {
     switch (log2n) {   // complex length N = n / 2
-        case 15: return pipe2_real_kernel<256, 128, 16, 32>();
+        case 15: return pipe2_real_kernel<128, 256, 32, 16>();
         case 16: return pipe2_real_kernel<256, 256, 16, 16>();
-        case 17: return pipe2_real_kernel<512, 256, 8, 16>();
+        case 17: return pipe2_real_kernel<256, 512, 16, 8>();
         case 18: return pipe2_real_kernel<512, 512, 8, 8>();
         default: return PipeChoice{};
     }
