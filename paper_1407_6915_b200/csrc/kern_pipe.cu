@@ -48,16 +48,17 @@ static PipeChoice pipe2_real_kernel() {
 }
 // the default k_pipe2 configurations with the C2R merge fused into the A-task
 // read (RS = 2: inverse real records of 2 N1 N2 samples)
-template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP, int NGRP>
+template <int N1, int N2, int COLS, int ROWS, int NSTAGE, int PP, int NGRP, int TWM = TW_SPLIT, int CB = 1>
 static PipeChoice pipe2_real_inv_kernel() {
-    PipeChoice ch = pipe2_kernel<N1, N2, COLS, ROWS, NSTAGE, PP, TW_SPLIT, NGRP>(true);
-    ch.k.fn = (const void*)&k_pipe2<N1, N2, COLS, ROWS, true, NSTAGE, PP, TW_SPLIT, NGRP, 1, false, 1, 2>;
+    PipeChoice ch = pipe2_kernel<N1, N2, COLS, ROWS, NSTAGE, PP, TWM, NGRP, CB>(true);
+    ch.k.fn = (const void*)&k_pipe2<N1, N2, COLS, ROWS, true, NSTAGE, PP, TWM, NGRP, CB, false, 1, 2>;
     return ch;
 }
 PipeChoice pick_pipe_real_inv(int log2n) {
     switch (log2n) {   // complex length N = n / 2; the configurations pick_pipe ships
         case 15: return pipe2_real_inv_kernel<128, 256, 32, 16, 3, 32, 2>();
         case 16: return pipe2_real_inv_kernel<256, 256, 16, 16, 3, 32, 2>();
+        // (256 x 512 with table twiddles and batched claims measured slower here: 27.8 / 33.7 %)
         case 17: return pipe2_real_inv_kernel<512, 256, 8, 16, 3, 32, 2>();
         case 18: return pipe2_real_inv_kernel<512, 512, 16, 16, 3, 32, 2>();
         default: return PipeChoice{};   // longer: two kernels measured faster (the partner reads miss L2)
