@@ -40,7 +40,8 @@ using namespace bfft;
 
 namespace {
 
-constexpr int TT = 32;   // tile edge
+constexpr int TT = 64;   // tile edge (512-byte runs both ways)
+constexpr int TY = 16;   // tile rows per thread pass
 
 struct Tw2 {   // W_N^m (or its conjugate for the inverse) = hi[m >> lb] * lo[m & mask]
     const float2* hi;
@@ -57,7 +58,7 @@ struct Tw2 {   // W_N^m (or its conjugate for the inverse) = hi[m >> lb] * lo[m 
 // `in` (row-major) goes to dst(r, c), consecutive r landing at consecutive
 // addresses; MUL multiplies by tw((gc0 + c) * r) first (pack2).
 template <int STEP>
-__global__ void __launch_bounds__(TT * 8) k_dist_pack(const float2* __restrict__ in, int64_t rows, int64_t cols,
+__global__ void __launch_bounds__(TT * TY) k_dist_pack(const float2* __restrict__ in, int64_t rows, int64_t cols,
                                                      float2* const* __restrict__ dst, int64_t R, int64_t C,
                                                      int64_t N1, int64_t N2, int me, Tw2 tw) {
     __shared__ float2 tile[TT][TT + 1];
@@ -74,16 +75,25 @@ __global__ void __launch_bounds__(TT * 8) k_dist_pack(const float2* __restrict__
             }
         }
         __syncthreads();
-        for (int i = threadIdx.y; i < TT; i += blockDim.y) {       // store along the destination rows
-            const int64_t c = c0 + i, r = r0 + threadIdx.x;
-            if (r >= rows || c >= cols) continue;
-            const float2 v = tile[threadIdx.x][i];
-            if (STEP == 1) {          // x slab [R][N2] (n1 = me R + r, n2 = c) -> A_{c/C}[c mod C][n1]
-                dst[c / C][(c % C) * N1 + me * R + r] = v;
-            } else if (STEP == 2) {   // A [C][N1] (n2 = me C + r, k1 = c) -> B_{k1/R}[k1 mod R][n2]
-                dst[c / R][(c % R) * N2 + me * C + r] = v;
-            } else {                  // B [R][N2] (k1 = me R + r, k2 = c) -> out_{k2/C}[(k2 mod C) N1 + k1]
-                dst[c / C][(c % C) * N1 + me * R + r] = v;
+        // destination GPU = c / DIV, row (c mod DIV) of stride STR, column OFF + r:
+        //   step 1: x slab [R][N2] (n1 = me R + r, n2 = c) -> A_{c/C}[c mod C][n1]
+        //   step 2: A [C][N1] (n2 = me C + r, k1 = c)     -> B_{k1/R}[k1 mod R][n2]
+        //   step 3: B [R][N2] (k1 = me R + r, k2 = c)     -> out_{k2/C}[(k2 mod C) N1 + k1]
+        // When DIV is a multiple of TT a tile's columns share one GPU: one 64-bit
+        // division per tile instead of per element (it bound the kernel near 2.6 TB/s).
+        const int64_t DIV = STEP == 2 ? R : C, STR = STEP == 2 ? N2 : N1;
+        const int64_t OFF = STEP == 2 ? (int64_t)me * C : (int64_t)me * R;
+        if (DIV % TT == 0) {
+            const int64_t gd = c0 / DIV, cm0 = c0 - gd * DIV;
+            float2* __restrict__ d = dst[gd] + OFF + r0 + threadIdx.x;
+            if (r0 + threadIdx.x < rows)
+                for (int i = threadIdx.y; i < TT; i += blockDim.y)
+                    if (c0 + i < cols) d[(cm0 + i) * STR] = tile[threadIdx.x][i];
+        } else {
+            for (int i = threadIdx.y; i < TT; i += blockDim.y) {   // store along the destination rows
+                const int64_t c = c0 + i, r = r0 + threadIdx.x;
+                if (r >= rows || c >= cols) continue;
+                dst[c / DIV][(c % DIV) * STR + OFF + r] = tile[threadIdx.x][i];
             }
         }
     }
@@ -298,10 +308,10 @@ extern "C" int fft_dplan_exec(fft_dplan* p, void* const* in, void* const* out) {
     const Tw2 tw{nullptr, nullptr, p->lb, (uint64_t)(p->n - 1)};
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->dev[0]);
-    const dim3 blk(TT, 8);
+    const dim3 blk(TT, TY);
     auto grid_for = [&](int64_t rows, int64_t cols) {
         const int64_t t = ((rows + TT - 1) / TT) * ((cols + TT - 1) / TT);
-        return (unsigned)std::min<int64_t>(t, (int64_t)sms * 8);
+        return (unsigned)std::min<int64_t>(t, (int64_t)sms * 2);
     };
     cudaError_t e;
     // inputs must be readable before anyone writes: start every stream after the caller's work
