@@ -40,8 +40,10 @@ using namespace bfft;
 
 namespace {
 
-constexpr int TT = 64;   // tile edge (512-byte runs both ways)
-constexpr int TY = 16;   // tile rows per thread pass
+// transpose tiles: TR source rows x TC source columns; a row is read as a
+// TC*8-byte run, a destination row written as a TR*8-byte run
+constexpr int TR = 256, TC = 64, PACK_THREADS = 1024;
+constexpr size_t PACK_SMEM = sizeof(float2) * TR * (TC + 1);
 
 struct Tw2 {   // W_N^m (or its conjugate for the inverse) = hi[m >> lb] * lo[m & mask]
     const float2* hi;
@@ -56,44 +58,57 @@ struct Tw2 {   // W_N^m (or its conjugate for the inverse) = hi[m >> lb] * lo[m 
 
 // Generic tile transpose: element (r, c) of the local [rows][cols] matrix
 // `in` (row-major) goes to dst(r, c), consecutive r landing at consecutive
-// addresses; MUL multiplies by tw((gc0 + c) * r) first (pack2).
+// addresses; step 2 multiplies by tw((me C + r) * c) first.  Tiles are
+// TR x TC (TC*8-byte reads, TR*8-byte writes); when the destination split
+// DIV is a multiple of TC a tile's columns share one GPU, so the destination
+// is resolved once per tile (a 64-bit division per element held the kernel
+// near 2.6 TB/s).
 template <int STEP>
-__global__ void __launch_bounds__(TT * TY) k_dist_pack(const float2* __restrict__ in, int64_t rows, int64_t cols,
-                                                     float2* const* __restrict__ dst, int64_t R, int64_t C,
-                                                     int64_t N1, int64_t N2, int me, Tw2 tw) {
-    __shared__ float2 tile[TT][TT + 1];
-    const int64_t tiles_c = (cols + TT - 1) / TT, tiles_r = (rows + TT - 1) / TT;
+__global__ void __launch_bounds__(PACK_THREADS, 1) k_dist_pack(const float2* __restrict__ in, int64_t rows,
+                                                             int64_t cols, float2* const* __restrict__ dst,
+                                                             int64_t R, int64_t C, int64_t N1, int64_t N2, int me,
+                                                             Tw2 tw) {
+    extern __shared__ float2 tile[];   // [TR][TC + 1]
+    const int l = threadIdx.x;
+    const int64_t tiles_c = (cols + TC - 1) / TC, tiles_r = (rows + TR - 1) / TR;
+    //   step 1: x slab [R][N2] (n1 = me R + r, n2 = c) -> A_{c/C}[c mod C][n1]
+    //   step 2: A [C][N1] (n2 = me C + r, k1 = c)     -> B_{k1/R}[k1 mod R][n2]
+    //   step 3: B [R][N2] (k1 = me R + r, k2 = c)     -> out_{k2/C}[(k2 mod C) N1 + k1]
+    const int64_t DIV = STEP == 2 ? R : C, STR = STEP == 2 ? N2 : N1;
+    const int64_t OFF = STEP == 2 ? (int64_t)me * C : (int64_t)me * R;
     for (int64_t t = blockIdx.x; t < tiles_r * tiles_c; t += gridDim.x) {
-        const int64_t r0 = (t / tiles_c) * TT, c0 = (t % tiles_c) * TT;
+        const int64_t r0 = (t / tiles_c) * TR, c0 = (t % tiles_c) * TC;
         __syncthreads();
-        for (int i = threadIdx.y; i < TT; i += blockDim.y) {       // load along the source rows
-            const int64_t r = r0 + i, c = c0 + threadIdx.x;
-            if (r < rows && c < cols) {
-                float2 v = __ldcs(in + r * cols + c);
-                if (STEP == 2) v = cmul(v, tw((uint64_t)(me * C + r) * (uint64_t)c));   // W^{n2 k1}, n2 = gC + r
-                tile[i][threadIdx.x] = v;
+        {   // load along the source rows: TC consecutive columns per row
+            const int cc = l % TC;
+            const int64_t c = c0 + cc;
+#pragma unroll 4
+            for (int rr = l / TC; rr < TR; rr += PACK_THREADS / TC) {
+                const int64_t r = r0 + rr;
+                if (r < rows && c < cols) {
+                    float2 v = __ldcs(in + r * cols + c);
+                    if (STEP == 2) v = cmul(v, tw((uint64_t)(me * C + r) * (uint64_t)c));   // W^{n2 k1}
+                    tile[rr * (TC + 1) + cc] = v;
+                }
             }
         }
         __syncthreads();
-        // destination GPU = c / DIV, row (c mod DIV) of stride STR, column OFF + r:
-        //   step 1: x slab [R][N2] (n1 = me R + r, n2 = c) -> A_{c/C}[c mod C][n1]
-        //   step 2: A [C][N1] (n2 = me C + r, k1 = c)     -> B_{k1/R}[k1 mod R][n2]
-        //   step 3: B [R][N2] (k1 = me R + r, k2 = c)     -> out_{k2/C}[(k2 mod C) N1 + k1]
-        // When DIV is a multiple of TT a tile's columns share one GPU: one 64-bit
-        // division per tile instead of per element (it bound the kernel near 2.6 TB/s).
-        const int64_t DIV = STEP == 2 ? R : C, STR = STEP == 2 ? N2 : N1;
-        const int64_t OFF = STEP == 2 ? (int64_t)me * C : (int64_t)me * R;
-        if (DIV % TT == 0) {
-            const int64_t gd = c0 / DIV, cm0 = c0 - gd * DIV;
-            float2* __restrict__ d = dst[gd] + OFF + r0 + threadIdx.x;
-            if (r0 + threadIdx.x < rows)
-                for (int i = threadIdx.y; i < TT; i += blockDim.y)
-                    if (c0 + i < cols) d[(cm0 + i) * STR] = tile[threadIdx.x][i];
-        } else {
-            for (int i = threadIdx.y; i < TT; i += blockDim.y) {   // store along the destination rows
-                const int64_t c = c0 + i, r = r0 + threadIdx.x;
-                if (r >= rows || c >= cols) continue;
-                dst[c / DIV][(c % DIV) * STR + OFF + r] = tile[threadIdx.x][i];
+        {   // store along the destination rows: TR consecutive r per destination row
+            const int rr = l % TR;
+            const int64_t r = r0 + rr;
+            if (r < rows) {
+                if (DIV % TC == 0) {
+                    const int64_t gd = c0 / DIV, cm0 = c0 - gd * DIV;
+                    float2* __restrict__ d = dst[gd] + OFF + r;
+#pragma unroll 4
+                    for (int cc = l / TR; cc < TC; cc += PACK_THREADS / TR)
+                        if (c0 + cc < cols) d[(cm0 + cc) * STR] = tile[rr * (TC + 1) + cc];
+                } else {
+                    for (int cc = l / TR; cc < TC; cc += PACK_THREADS / TR) {
+                        const int64_t c = c0 + cc;
+                        if (c < cols) dst[c / DIV][(c % DIV) * STR + OFF + r] = tile[rr * (TC + 1) + cc];
+                    }
+                }
             }
         }
     }
@@ -245,6 +260,9 @@ extern "C" fft_dplan* fft_dplan_create(int64_t n, int ngpu, const int* devices, 
         DTRY(cudaMemcpy(p->hi[g], thi.data(), nhi * sizeof(float2), cudaMemcpyHostToDevice));
         DTRY(cudaMemcpy(p->lo[g], tlo.data(), nlo * sizeof(float2), cudaMemcpyHostToDevice));
         DTRY(cudaMalloc(&p->dst[g], 3 * ngpu * sizeof(float2*)));
+        DTRY(cudaFuncSetAttribute(k_dist_pack<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
+        DTRY(cudaFuncSetAttribute(k_dist_pack<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
+        DTRY(cudaFuncSetAttribute(k_dist_pack<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
         DTRY(cudaStreamCreateWithFlags(&p->st[g], cudaStreamNonBlocking));
         DTRY(cudaEventCreateWithFlags(&p->ev[g], cudaEventDisableTiming));
         p->p1[g] = fft_plan_create(n1, n2 / ngpu, dir);   // C column records of N1 points
@@ -308,10 +326,10 @@ extern "C" int fft_dplan_exec(fft_dplan* p, void* const* in, void* const* out) {
     const Tw2 tw{nullptr, nullptr, p->lb, (uint64_t)(p->n - 1)};
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->dev[0]);
-    const dim3 blk(TT, TY);
+    const dim3 blk(PACK_THREADS);
     auto grid_for = [&](int64_t rows, int64_t cols) {
-        const int64_t t = ((rows + TT - 1) / TT) * ((cols + TT - 1) / TT);
-        return (unsigned)std::min<int64_t>(t, (int64_t)sms * 2);
+        const int64_t t = ((rows + TR - 1) / TR) * ((cols + TC - 1) / TC);
+        return (unsigned)std::min<int64_t>(t, (int64_t)sms);
     };
     cudaError_t e;
     // inputs must be readable before anyone writes: start every stream after the caller's work
@@ -329,7 +347,7 @@ extern "C" int fft_dplan_exec(fft_dplan* p, void* const* in, void* const* out) {
     // ---- step 1: transpose + all-to-all into A
     for (int g = 0; g < G; ++g) {
         cudaSetDevice(p->dev[g]);
-        k_dist_pack<1><<<grid_for(R, p->n2), blk, 0, p->st[g]>>>((const float2*)in[g], R, p->n2, p->dst[g], R, C,
+        k_dist_pack<1><<<grid_for(R, p->n2), blk, PACK_SMEM, p->st[g]>>>((const float2*)in[g], R, p->n2, p->dst[g], R, C,
                                                                  p->n1, p->n2, g, tw);
         if ((e = cudaGetLastError()) != cudaSuccess) return err(e, "pack kernel launch");
     }
@@ -346,7 +364,7 @@ extern "C" int fft_dplan_exec(fft_dplan* p, void* const* in, void* const* out) {
     for (int g = 0; g < G; ++g) {
         cudaSetDevice(p->dev[g]);
         const Tw2 t{p->hi[g], p->lo[g], p->lb, (uint64_t)(p->n - 1)};
-        k_dist_pack<2><<<grid_for(C, p->n1), blk, 0, p->st[g]>>>(p->a[g], C, p->n1, p->dst[g] + G, R, C, p->n1,
+        k_dist_pack<2><<<grid_for(C, p->n1), blk, PACK_SMEM, p->st[g]>>>(p->a[g], C, p->n1, p->dst[g] + G, R, C, p->n1,
                                                                  p->n2, g, t);
         if ((e = cudaGetLastError()) != cudaSuccess) return err(e, "pack kernel launch");
     }
@@ -363,7 +381,7 @@ extern "C" int fft_dplan_exec(fft_dplan* p, void* const* in, void* const* out) {
     if ((e = barrier()) != cudaSuccess) return err(e, "cross-GPU ordering");
     for (int g = 0; g < G; ++g) {
         cudaSetDevice(p->dev[g]);
-        k_dist_pack<3><<<grid_for(R, p->n2), blk, 0, p->st[g]>>>(p->b[g], R, p->n2, p->dst[g] + 2 * G, R, C,
+        k_dist_pack<3><<<grid_for(R, p->n2), blk, PACK_SMEM, p->st[g]>>>(p->b[g], R, p->n2, p->dst[g] + 2 * G, R, C,
                                                                  p->n1, p->n2, g, tw);
         if ((e = cudaGetLastError()) != cudaSuccess) return err(e, "pack kernel launch");
     }
