@@ -44,9 +44,11 @@ __global__ void __launch_bounds__(256) k_real_split(const float2* __restrict__ i
                                                      int64_t nrec, int64_t h, const float2* __restrict__ hi,
                                                      const float2* __restrict__ lo, int lb) {
     const int64_t pairs = h / 2 + 1;   // k = 0 .. h/2
-    const int64_t total = nrec * pairs;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / pairs, k = i - r * pairs;
+    // a block takes 256 consecutive k of one record: one division per block, not per element
+    const int64_t bpr = (pairs + 255) / 256;
+    for (int64_t bt = blockIdx.x; bt < nrec * bpr; bt += gridDim.x) {
+        const int64_t r = bt / bpr, k = (bt - r * bpr) * 256 + threadIdx.x;
+        if (k >= pairs) continue;
         const float2* src = in + r * h;
         float2* dst = out + r * h;
         if (k == 0) {
