@@ -440,8 +440,9 @@ k_fs_rows(const float2* __restrict__ y, float2* __restrict__ out, int64_t nrec, 
 static __global__ void k_frames(const float2* __restrict__ in, float2* __restrict__ out, int64_t frames, int64_t n,
                                 int64_t hop, const float* __restrict__ window) {
     const int64_t total = frames * n;
+    const int lg = __ffsll((unsigned long long)n) - 1;   // n is a power of two: shift, not a 64-bit division
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t f = i / n, j = i - f * n;
+        const int64_t f = i >> lg, j = i & (n - 1);
         float2 x = __ldcs(in + f * hop + j);
         if (window) {
             const float w = __ldg(window + j);
