@@ -2,7 +2,7 @@
 import ctypes, os, sys, math, json
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
-lib = ctypes.CDLL(os.path.join(ROOT, "tools", "exp", "libgen.so"))
+lib = ctypes.CDLL(os.path.join(ROOT, "tools", "exp", os.environ.get("EXP_LIB", "libgen.so")))
 vp, i32 = ctypes.c_void_p, ctypes.c_int
 lib.exp_run.argtypes = [i32, vp, vp, vp, vp, ctypes.c_longlong, i32, vp, vp, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]
 lib.exp_run.restype = ctypes.c_float
