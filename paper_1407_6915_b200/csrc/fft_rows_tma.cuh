@@ -34,12 +34,31 @@ __device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uin
         : "memory");
 }
 
+// Exchange layout of the staged kernels: RowLayout (one pad entry per 16)
+// plus, for engines whose second pass writes groups of Ns < 16 consecutive
+// outputs G = Ns * R entries apart (2^13 with radix-32: Ns = 8, G = 256), 8 pad
+// entries per G, which puts neighbouring groups on opposite bank halves
+// (k_rows_tma at 2^13 spent 37 % of its store wavefronts on conflicts,
+// profiles/r02_rows_tma_2p13_ncu.md; with the extra pad 82.7 vs 80.6 % on one
+// box, profiles/r02_rows_tma.txt).
+template <int L, int PP>
+struct TmaLayout {
+    using S = Sched<L, PP>;
+    static constexpr int NS1 = S::NPASS > 2 ? S::ns(1) : 16;    // outputs per group in pass 1
+    static constexpr int G = NS1 < 16 ? NS1 * S::radix(1) : 0;  // group spacing (0: no extra pad)
+    __device__ __forceinline__ static int at(int e) {
+        if constexpr (G > 0) return e + (e >> 4) + 8 * (e / G);
+        else return RowLayout::at(e);
+    }
+    __host__ __device__ static constexpr int size(int n) { return RowLayout::size(n) + (G > 0 ? 8 * (n / G) : 0); }
+};
+
 template <int L, int PP, int NGRP, int NSTAGE>
 struct RowsTmaCfg {
     using S = Sched<L, PP>;
     static constexpr int T = S::T;                                     // threads per record (one group)
     static constexpr int NT = NGRP * T;
-    static constexpr int STAGE = (RowLayout::size(L) + 15) / 16 * 16;  // entries per stage (padded exchanges)
+    static constexpr int STAGE = (TmaLayout<L, PP>::size(L) + 15) / 16 * 16;  // entries per stage (padded exchanges)
     static constexpr int CHUNKS = L * 8 >= 4 * 16384 ? 4 : 1;          // bulk copies per record
     static constexpr size_t SMEM = sizeof(float2) * (size_t)STAGE * NSTAGE + 8 * NSTAGE;
     static constexpr int MINB = SMEM * 2 <= 227 * 1024 ? 2 : 1;
@@ -123,7 +142,7 @@ k_rows_tma(const float2* __restrict__ in, float2* __restrict__ out, int64_t nrec
                     v[j] = INV ? conjf2(x) : x;
                 }
             }
-            fft_engine<L, PP>(v, t, stage, [](int e) { return RowLayout::at(e); }, tab, bar);
+            fft_engine<L, PP>(v, t, stage, [](int e) { return TmaLayout<L, PP>::at(e); }, tab, bar);
             float2* dst = out + r * L + t;
             if constexpr (REAL == 1) {
                 // X[k] = E + W_n^k O, E = (Z[k] + conj Z[L-k]) / 2, O = (Z[k] - conj Z[L-k]) / (2i); out[0] = (X[0], X[L])
