@@ -162,7 +162,7 @@ __device__ __forceinline__ void twiddle_row16(uint32_t m0, uint32_t dm, uint32_t
 template <int L, int B, int PP = 16>
 struct RowsMinBlocks {  // CTAs per SM the register budget is sized for
     static constexpr int THREADS = B * Sched<L, PP>::T;
-    static constexpr int V = PP == 32 ? (THREADS <= 256 ? 2 : 1) : (THREADS <= 256 ? 3 : 1);
+    static constexpr int V = PP == 32 ? (THREADS <= 256 ? 2 : 1) : (THREADS <= 256 ? 4 : 1);
 };
 
 // W_64^j = exp(-2 pi i j / 64), j = 0..63, fp64-computed and rounded to fp32

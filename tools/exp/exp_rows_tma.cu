@@ -12,8 +12,8 @@ template <int L, int PP, int NGRP, int NST> static Cfg mk(const char* name) {
     using CF = RowsTmaCfg<L, PP, NGRP, NST>;
     return Cfg{(const void*)&k_rows_tma<L, false, PP, NGRP, NST>, CF::NT, CF::SMEM, L, PP, name, 1};
 }
-template <int L, int PP, int B> static Cfg mkr(const char* name) {
-    return Cfg{(const void*)&k_rows<L, B, false, PP>, B * Sched<L, PP>::T, sizeof(float2) * RowLayout::size(B * L), L, PP, name, 0};
+template <int L, int PP, int B, int MINB = 0> static Cfg mkr(const char* name) {
+    return Cfg{(const void*)&k_rows<L, B, false, PP, MINB>, B * Sched<L, PP>::T, sizeof(float2) * RowLayout::size(B * L), L, PP, name, 0};
 }
 static Cfg table(int i) {
     switch (i) {
@@ -43,10 +43,21 @@ static Cfg table(int i) {
         case 23: return mk2<16384, 16, 10240>("tma2 2^14 p16 head 10240");
         case 24: return mk2<8192, 32, 4096>("tma2 2^13 p32 head 4096");
         case 25: return mk2<8192, 16, 4096>("tma2 2^13 p16 head 4096");
+        case 26: return mkr<512, 16, 8, 4>("k_rows 2^9 minb4");
+        case 27: return mkr<1024, 16, 4, 4>("k_rows 2^10 minb4");
+        case 28: return mkr<2048, 16, 2, 4>("k_rows 2^11 minb4");
+        case 29: return mkr<4096, 16, 1, 4>("k_rows 2^12 minb4");
+        case 30: return mkr<1024, 16, 4, 5>("k_rows 2^10 minb5");
+        case 31: return mkr<512, 16, 8, 3>("k_rows 2^9 minb3");
+        case 32: return mkr<1024, 16, 4, 3>("k_rows 2^10 minb3");
+        case 33: return mkr<2048, 16, 2, 3>("k_rows 2^11 minb3");
+        case 34: return mkr<4096, 16, 1, 3>("k_rows 2^12 minb3");
+        case 35: return mkr<256, 16, 16, 3>("k_rows 2^8 minb3");
+        case 36: return mkr<256, 16, 16, 4>("k_rows 2^8 minb4");
         default: return Cfg{nullptr};
     }
 }
-extern "C" int exp_ncfg() { return 26; }
+extern "C" int exp_ncfg() { return 37; }
 extern "C" const char* exp_name(int i) { return table(i).name; }
 extern "C" int exp_L(int i) { return table(i).L; }
 extern "C" int exp_pp(int i) { return table(i).pp; }
