@@ -37,10 +37,12 @@ static Cfg table(int i) {
         case 16: return mk<16, 16, 6, 32, TW_SPLIT, 4, 2>("c16 s6 g4 cb2");
         case 17: return mk<16, 16, 6, 32, TW_SPLIT, 3, 4>("c16 s6 g3 cb4");
         case 18: return mk<16, 16, 3, 32, TW_SPLIT, 2, 2>("c16 s3 g2 cb2");
+        case 19: return mk<16, 16, 3, 32, TW_SPLIT, 2, 1, true>("c16 s3 g2 pf");
+        case 20: return mk<16, 16, 3, 32, TW_SPLIT, 2, 2, true>("c16 s3 g2 cb2 pf");
         default: return Cfg{nullptr, 0, 0, 0, 0, 0, 0, 0, 0, nullptr, 1, 1};
     }
 }
-extern "C" int exp_ncfg() { return 19; }
+extern "C" int exp_ncfg() { return 21; }
 // the constant-memory Stockham twiddles of this translation unit (same table as plan.cu builds)
 static void stockham_table(int L, std::vector<float2>& out, int P) {
     out.clear();
